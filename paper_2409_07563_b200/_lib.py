@@ -1,0 +1,112 @@
+"""Loads the in-tree CUDA library (libsmpc_b200.so) and declares the C ABI.
+
+There is no fallback: if the library is missing or no CUDA device is usable,
+``load()`` raises. The product path never routes through the CPU oracle.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from .scenario import SmpcProblem, SmpcSolution, SmpcTubeSolution, SmpcWeightSummary
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libsmpc_b200.so")
+
+# Every symbol include/smpc_b200.h declares (checked by tests/test_capi_symbols.py).
+EXPORTED = [
+    "smpc_create", "smpc_destroy", "smpc_last_error", "smpc_error_location", "smpc_get_dims",
+    "smpc_set_mean", "smpc_get_mean", "smpc_compute_control", "smpc_tube_compute_control",
+    "smpc_shift_control_sequence", "smpc_get_solve_count", "smpc_set_solve_count",
+    "smpc_generate_samples", "smpc_rollout", "smpc_compute_weights", "smpc_set_x0",
+    "smpc_launch_iteration", "smpc_synchronize", "smpc_stream", "smpc_kernels_per_solve",
+    "smpc_rollout_kernel_ms", "smpc_comm_unique_id", "smpc_comm_init", "smpc_host_libm_uses_fma",
+    "smpc_measure_fp32_peak", "smpc_version",
+]
+
+_lib = None
+
+
+class SmpcError(RuntimeError):
+    """smpc::Error — message text matches the reference's exception."""
+
+    def __init__(self, status: int, message: str, sample=-1, timestep=-1, channel=-1):
+        super().__init__(message)
+        self.status = status
+        self.sample, self.timestep, self.channel = sample, timestep, channel
+
+
+class SmpcConfigError(SmpcError):
+    """smpc::ConfigError."""
+
+
+def load(path: str = LIB_PATH) -> ctypes.CDLL:
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+                          " (there is no CPU fallback)")
+    L = ctypes.CDLL(path)
+    P = ctypes.POINTER
+    c_ctx = ctypes.c_void_p
+    f32p = np.ctypeslib.ndpointer(np.float32, flags="C_CONTIGUOUS")
+    f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
+    u8p = np.ctypeslib.ndpointer(np.uint8, flags="C_CONTIGUOUS")
+    L.smpc_create.argtypes = [P(SmpcProblem), P(c_ctx)]
+    L.smpc_destroy.argtypes = [c_ctx]
+    L.smpc_destroy.restype = None
+    L.smpc_last_error.argtypes = [c_ctx]
+    L.smpc_last_error.restype = ctypes.c_char_p
+    L.smpc_error_location.argtypes = [c_ctx, P(ctypes.c_int64), P(ctypes.c_int32), P(ctypes.c_int32)]
+    L.smpc_get_dims.argtypes = [c_ctx, P(ctypes.c_int32), P(ctypes.c_int32), P(ctypes.c_int32)]
+    L.smpc_set_mean.argtypes = [c_ctx, ctypes.c_int32, f32p]
+    L.smpc_get_mean.argtypes = [c_ctx, ctypes.c_int32, f32p]
+    L.smpc_compute_control.argtypes = [c_ctx, f32p, P(SmpcSolution)]
+    L.smpc_tube_compute_control.argtypes = [c_ctx, f32p, P(SmpcTubeSolution)]
+    L.smpc_shift_control_sequence.argtypes = [c_ctx, ctypes.c_double, ctypes.c_double]
+    L.smpc_get_solve_count.argtypes = [c_ctx, P(ctypes.c_uint64)]
+    L.smpc_set_solve_count.argtypes = [c_ctx, ctypes.c_uint64]
+    L.smpc_generate_samples.argtypes = [c_ctx, f32p, ctypes.c_uint32, f32p, ctypes.c_void_p]
+    L.smpc_rollout.argtypes = [c_ctx, ctypes.c_int32, f32p, f32p, ctypes.c_void_p, ctypes.c_uint32, f64p,
+                               ctypes.c_void_p]
+    L.smpc_compute_weights.argtypes = [c_ctx, f64p, ctypes.c_int64, ctypes.c_double, ctypes.c_void_p,
+                                       P(SmpcWeightSummary)]
+    L.smpc_set_x0.argtypes = [c_ctx, f32p]
+    L.smpc_launch_iteration.argtypes = [c_ctx]
+    L.smpc_synchronize.argtypes = [c_ctx]
+    L.smpc_stream.argtypes = [c_ctx]
+    L.smpc_stream.restype = ctypes.c_void_p
+    L.smpc_kernels_per_solve.argtypes = [c_ctx]
+    L.smpc_kernels_per_solve.restype = ctypes.c_int32
+    L.smpc_rollout_kernel_ms.argtypes = [c_ctx, ctypes.c_int32, P(ctypes.c_double), P(ctypes.c_int64)]
+    L.smpc_comm_unique_id.argtypes = [ctypes.c_char_p]
+    L.smpc_comm_init.argtypes = [c_ctx, ctypes.c_char_p, ctypes.c_int32, ctypes.c_int32]
+    L.smpc_host_libm_uses_fma.argtypes = []
+    L.smpc_host_libm_uses_fma.restype = ctypes.c_int32
+    L.smpc_measure_fp32_peak.argtypes = [ctypes.c_int32, P(ctypes.c_double)]
+    L.smpc_measure_fp32_peak.restype = ctypes.c_int
+    L.smpc_version.argtypes = []
+    L.smpc_version.restype = ctypes.c_char_p
+    for name in ["smpc_create", "smpc_error_location", "smpc_get_dims", "smpc_set_mean", "smpc_get_mean",
+                 "smpc_compute_control", "smpc_tube_compute_control", "smpc_shift_control_sequence",
+                 "smpc_get_solve_count", "smpc_set_solve_count", "smpc_generate_samples", "smpc_rollout",
+                 "smpc_compute_weights", "smpc_set_x0", "smpc_launch_iteration", "smpc_synchronize",
+                 "smpc_rollout_kernel_ms", "smpc_comm_unique_id", "smpc_comm_init"]:
+        getattr(L, name).restype = ctypes.c_int
+    _lib = L
+    return L
+
+
+def check(status: int, ctx=None) -> None:
+    if status == 0:
+        return
+    L = load()
+    msg = (L.smpc_last_error(ctx) or b"").decode()
+    sample, t, ch = ctypes.c_int64(-1), ctypes.c_int32(-1), ctypes.c_int32(-1)
+    if ctx:
+        L.smpc_error_location(ctx, ctypes.byref(sample), ctypes.byref(t), ctypes.byref(ch))
+    cls = SmpcConfigError if status == 2 else SmpcError
+    raise cls(status, msg, sample.value, t.value, ch.value)

@@ -1,0 +1,140 @@
+// Host/device launch descriptors shared by the kernel instantiation units and
+// the C-ABI host code. Plain PODs: the host fills them once per context and
+// the kernels read them as by-value kernel parameters.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace smpc_dev {
+
+constexpr int kMaxNX = 8;
+constexpr int kMaxNU = 4;
+constexpr int kMaxNY = 8;
+constexpr int kRolloutThreads = 128;
+constexpr int kUpdateThreads = 256;
+constexpr int kUpdateWarps = kUpdateThreads / 32;
+
+// Error key (lowest key wins = what a single-worker reference would throw):
+//   [63:62] stage  0 rollout, 1 compute_weights, 2 finish_solution
+//   [61]    system
+//   [60:30] sample (global index)
+//   [29:6]  timestep
+//   [5:4]   phase  0 non-finite state, 1 invalid running cost, 2 terminal
+//   [3:0]   channel
+constexpr unsigned long long kNoError = ~0ull;
+__host__ __device__ inline unsigned long long make_error_key(unsigned stage, unsigned s, long long m,
+                                                             int t, unsigned phase, unsigned ch) {
+  return ((unsigned long long)stage << 62) | ((unsigned long long)(s & 1) << 61) |
+         ((unsigned long long)(m & 0x7fffffffLL) << 30) | ((unsigned long long)(t & 0xffffff) << 6) |
+         ((unsigned long long)(phase & 3) << 4) | (unsigned long long)(ch & 15);
+}
+
+// Model / cost parameters as plain floats (device functors are built from these).
+struct DynParams {
+  float p[8];
+};
+struct CostParams {
+  float p[8];
+  int n_quad;
+  float target[kMaxNY], weights[kMaxNY];
+  // costmap (diff_drive_nav)
+  const uint8_t* grid;  // device pointer
+  int cells_x, cells_y;
+  float origin_x, origin_y, inv_resolution;
+  int map_in_smem;
+};
+
+// Per-context iteration state on the device.
+struct ResultHeader {
+  unsigned long long err_key;
+  unsigned long long abort_key;
+  unsigned long long solve_count;
+  double rho[2];
+  double eta[2];
+  long long argmin[2];
+  long long nonzero[2];
+  float next_nominal_state[kMaxNX];
+};
+
+struct IterArgs {
+  // problem
+  int T, S;
+  int M_local;
+  long long m_begin;
+  long long M_global;
+  float dt;
+  double lambda;
+  uint32_t key0, key1;
+  int with_mean;
+  long long zero_begin;
+  int importance;
+  int world, rank;
+  // noise stream: stream = solve_count*256 + iter (stream_for, controllers.cpp:63-66),
+  // or the explicit value when solve_count == nullptr
+  const unsigned long long* solve_count;
+  int iter;
+  uint32_t stream;
+  // inputs
+  const float* mean_in;  // [S][T][NU]
+  float* mean_out;       // [S][T][NU]
+  const float* x0;       // [S][NX]
+  const float* sigma;    // [T][NU]
+  const double* sig2;    // [T][NU]
+  const double* gamma;   // [T]
+  const float* eps_in;   // injected [M_local][T][NU] or nullptr
+  const float* tail;     // Phi^-1 tail table
+  // rollout outputs
+  double* costs;   // [S][M_local]
+  float* outputs;  // [S][M_local][T][NY] or nullptr
+  // reduction scratch
+  int n_roll_blocks;
+  double* blk_min;       // [S][n_roll_blocks]
+  long long* blk_arg;    // [S][n_roll_blocks]
+  unsigned int* counters;  // [8] arrival counters (self-resetting)
+  double* gather1;       // [world][S][2]  (rho_g, argmin_g as double bits)
+  double* weights;       // [S][M_local] e_m (unnormalised) -> weights
+  int n_w_blocks;
+  double* blk_eta;       // [S][n_w_blocks]
+  long long* blk_nz;     // [S][n_w_blocks]
+  double* gather2;       // [world][S][2]  (eta_g, nonzero_g)
+  int n_u_blocks;
+  double* blk_part;      // [S][n_u_blocks][T*NU]
+  double* gather3;       // [world][S][T*NU]
+  // results
+  ResultHeader* header;
+  float* controls;  // [S][T][NU]
+  float* states;    // [S][T+1][NX]
+  float* outs_nom;  // [S][T][NY]
+  int do_finish;    // final iteration of a solve: nominal rollout + solve_count++
+  int normalize_weights;  // write w = e/eta back (only when the caller wants weights)
+  DynParams dyn;
+  CostParams cost;
+};
+
+// One set of launchers per (dynamics kind, libm variant); cost kind and S are
+// dispatched inside. Defined in inst_*.cu.
+struct ModelOps {
+  cudaError_t (*rollout)(const IterArgs&, int cost_kind, cudaStream_t);
+  cudaError_t (*weights)(const IterArgs&, cudaStream_t);
+  cudaError_t (*update)(const IterArgs&, cudaStream_t);
+  cudaError_t (*combine)(const IterArgs&, cudaStream_t);
+  cudaError_t (*generate)(const IterArgs&, float* eps_out, uint8_t* flags_out, cudaStream_t);
+  int nx, nu, ny;
+};
+
+ModelOps ops_unicycle(bool fma_libm);
+ModelOps ops_cartpole(bool fma_libm);
+ModelOps ops_diff_drive(bool fma_libm);
+ModelOps ops_double_integrator();
+
+cudaError_t build_tail_table(float* table, uint32_t n, cudaStream_t stream);
+cudaError_t launch_begin_solve(ResultHeader* h, cudaStream_t stream);
+cudaError_t launch_finish_solve(ResultHeader* h, cudaStream_t stream);
+cudaError_t launch_weights(const IterArgs& a, cudaStream_t stream);
+cudaError_t launch_normalize_weights(const IterArgs& a, cudaStream_t stream);
+cudaError_t launch_min_only(const double* costs, long long n, double* blk_min, long long* blk_arg,
+                            int nblk, unsigned int* counter, double* out_rho, long long* out_arg,
+                            cudaStream_t stream);
+
+}  // namespace smpc_dev

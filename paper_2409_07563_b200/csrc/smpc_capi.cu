@@ -1,0 +1,1070 @@
+// C-ABI implementation (include/smpc_b200.h): context lifecycle, validation
+// with the reference's error texts, device buffers, the captured per-solve
+// CUDA graph, the engine/sampler boundary calls and NCCL multi-GPU plumbing.
+// Host code only — all arithmetic on the hot path runs in the kernels.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <math.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "../../include/smpc_b200.h"
+#include "launch.h"
+
+using namespace smpc_dev;
+
+extern "C" int32_t smpc_host_libm_uses_fma(void);  // libm_probe.cpp
+
+namespace {
+
+thread_local std::string g_create_error;
+
+// ---- minimal NCCL surface, loaded with dlopen so single-GPU use never needs it
+typedef struct ncclComm* ncclComm_t;
+typedef struct {
+  char internal[128];
+} ncclUniqueId;
+typedef int ncclResult_t;
+enum { ncclInt8 = 0, ncclChar = 0, ncclUint8 = 1, ncclFloat64 = 8 };
+struct NcclApi {
+  void* handle = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi* nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    const char* names[] = {"libnccl.so.2", "libnccl.so",
+                           "/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl/lib/libnccl.so.2"};
+    for (const char* n : names) {
+      api.handle = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+      if (api.handle) break;
+    }
+    if (api.handle) {
+      api.GetUniqueId = (ncclResult_t(*)(ncclUniqueId*))dlsym(api.handle, "ncclGetUniqueId");
+      api.CommInitRank = (ncclResult_t(*)(ncclComm_t*, int, ncclUniqueId, int))dlsym(api.handle, "ncclCommInitRank");
+      api.AllGather = (ncclResult_t(*)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t))dlsym(
+          api.handle, "ncclAllGather");
+      api.CommDestroy = (ncclResult_t(*)(ncclComm_t))dlsym(api.handle, "ncclCommDestroy");
+      api.GetErrorString = (const char* (*)(ncclResult_t))dlsym(api.handle, "ncclGetErrorString");
+    }
+  }
+  return api.GetUniqueId ? &api : nullptr;
+}
+
+struct ConfigError {
+  std::string msg;
+};
+struct RuntimeError {
+  std::string msg;
+};
+struct CudaError {
+  std::string msg;
+};
+
+#define CK(call)                                                                      \
+  do {                                                                                \
+    cudaError_t e_ = (call);                                                          \
+    if (e_ != cudaSuccess) throw CudaError{std::string(#call) + ": " + cudaGetErrorString(e_)}; \
+  } while (0)
+
+template <typename T>
+T* dalloc(size_t n) {
+  if (n == 0) n = 1;
+  void* p = nullptr;
+  CK(cudaMalloc(&p, n * sizeof(T)));
+  CK(cudaMemset(p, 0, n * sizeof(T)));
+  return static_cast<T*>(p);
+}
+
+const char* controller_name(int kind) {
+  return kind == SMPC_CTRL_DMD ? "dmd" : kind == SMPC_CTRL_TUBE ? "tube" : "mppi";
+}
+
+}  // namespace
+
+struct smpc_ctx {
+  smpc_problem p{};
+  std::vector<float> std_per_step, step_sizes;
+  std::vector<uint8_t> costmap;
+  ModelOps ops{};
+  int nx = 0, nu = 0, ny = 0, S = 1, T = 0, I = 1;
+  long long M = 0, M_local = 0, m_begin = 0;
+  bool fma = true;
+  cudaStream_t stream = nullptr;
+  // device buffers
+  float *d_mean = nullptr, *d_x0 = nullptr, *d_sigma = nullptr, *d_tail = nullptr;
+  double *d_sig2 = nullptr, *d_gamma = nullptr, *d_costs = nullptr, *d_weights = nullptr;
+  double *d_blk_min = nullptr, *d_blk_eta = nullptr, *d_blk_part = nullptr;
+  double *d_gather1 = nullptr, *d_gather2 = nullptr, *d_gather3 = nullptr;
+  long long *d_blk_arg = nullptr, *d_blk_nz = nullptr;
+  unsigned int* d_counters = nullptr;
+  uint8_t* d_costmap = nullptr;
+  unsigned char* d_result = nullptr;
+  unsigned char* h_result = nullptr;  // pinned
+  size_t result_bytes = 0, off_controls = 0, off_states = 0, off_outs = 0;
+  float* h_x0 = nullptr;  // pinned staging
+  // scratch for the engine / sampler boundary
+  float *d_ro_x0 = nullptr, *d_ro_mean = nullptr, *d_eps = nullptr, *d_outputs = nullptr;
+  size_t eps_cap = 0, outputs_cap = 0;
+  double* d_wscratch = nullptr;
+  size_t wscratch_cap = 0;
+  uint8_t* d_flags = nullptr;
+  size_t flags_cap = 0;
+  IterArgs base{};
+  int n_roll_blocks = 1, n_w_blocks = 1, n_u_blocks = 1;
+  // graph
+  cudaGraphExec_t graph = nullptr;
+  bool timing = false;
+  std::vector<cudaEvent_t> ev;
+  double rollout_ms_total = 0.0;
+  long long rollout_launches = 0;
+  // multi-GPU
+  ncclComm_t comm = nullptr;
+  int rank = 0, world = 1;
+  // host state
+  uint64_t solve_count = 0;
+  std::string err;
+  long long err_sample = -1;
+  int err_t = -1, err_ch = -1;
+  std::vector<float> nominal_state;
+  bool nominal_started = false;
+  std::vector<float> host_mean[2];
+
+  ResultHeader* header() { return reinterpret_cast<ResultHeader*>(d_result); }
+  ResultHeader* h_header() { return reinterpret_cast<ResultHeader*>(h_result); }
+};
+
+namespace {
+
+void set_error(smpc_ctx* c, const std::string& msg) {
+  if (c) {
+    c->err = msg;
+    c->err_sample = -1;
+    c->err_t = -1;
+    c->err_ch = -1;
+  } else {
+    g_create_error = msg;
+  }
+}
+
+template <class F>
+smpc_status guarded(smpc_ctx* c, F&& f) {
+  try {
+    f();
+    return SMPC_OK;
+  } catch (const ConfigError& e) {
+    set_error(c, e.msg);
+    return SMPC_ERR_CONFIG;
+  } catch (const RuntimeError& e) {
+    set_error(c, e.msg);
+    return SMPC_ERR_RUNTIME;
+  } catch (const CudaError& e) {
+    set_error(c, e.msg);
+    return SMPC_ERR_CUDA;
+  } catch (const std::exception& e) {
+    set_error(c, e.what());
+    return SMPC_ERR_RUNTIME;
+  }
+}
+
+double pd(const smpc_problem& p, int i, double d) { return i < p.n_dyn_params ? p.dyn_params[i] : d; }
+double pc(const smpc_problem& p, int i, double d) { return i < p.n_cost_params ? p.cost_params[i] : d; }
+
+// Validation mirroring the reference constructors' checks and messages:
+// Controller ctor (controllers.cpp:23-49), GaussianSampler ctor
+// (sampling.cpp:7-30), model ctors (dynamics.cpp:133-171), cost ctors and
+// make_cost (costs.cpp:27-162), RolloutEngine::validate (engine.cpp:81-127).
+void validate(smpc_ctx* c) {
+  const smpc_problem& p = c->p;
+  if (p.abi_version != SMPC_B200_ABI_VERSION) throw ConfigError{"smpc_problem: ABI version mismatch"};
+  const std::string name = controller_name(p.controller_kind);
+  switch (p.dynamics_kind) {
+    case SMPC_DYN_UNICYCLE: c->ops = ops_unicycle(c->fma); break;
+    case SMPC_DYN_CARTPOLE:
+      if (!(pd(p, 0, 1) > 0) || !(pd(p, 1, 1) > 0) || !(pd(p, 2, 1) > 0) ||
+          !((float)pd(p, 0, 1) > 0.0f) || !((float)pd(p, 1, 1) > 0.0f) || !((float)pd(p, 2, 1) > 0.0f))
+        throw RuntimeError{"cartpole: masses and pole length must be > 0"};
+      c->ops = ops_cartpole(c->fma);
+      break;
+    case SMPC_DYN_DIFF_DRIVE:
+      if (!((float)pd(p, 0, 1) > 0.0f) || !((float)pd(p, 1, 1) > 0.0f))
+        throw RuntimeError{"diff_drive: wheel geometry must be > 0"};
+      if (!((float)pd(p, 2, -0.35) < (float)pd(p, 3, 0.5)))
+        throw RuntimeError{"diff_drive: control bound lower must be < upper on channel 0"};
+      if (!((float)pd(p, 4, -0.5) < (float)pd(p, 5, 0.5)))
+        throw RuntimeError{"diff_drive: control bound lower must be < upper on channel 1"};
+      c->ops = ops_diff_drive(c->fma);
+      break;
+    case SMPC_DYN_DOUBLE_INTEGRATOR: c->ops = ops_double_integrator(); break;
+    default: throw ConfigError{"dynamics.kind is not recognized"};
+  }
+  c->nx = c->ops.nx, c->nu = c->ops.nu, c->ny = c->ops.ny;
+  if (p.controller_kind != SMPC_CTRL_MPPI && p.controller_kind != SMPC_CTRL_DMD &&
+      p.controller_kind != SMPC_CTRL_TUBE)
+    throw ConfigError{"controller.kind is not recognized"};
+  // cost (make_cost + ctor checks)
+  int cost_ny = c->ny, cost_nu = c->nu;
+  std::string cost_name;
+  switch (p.cost_kind) {
+    case SMPC_COST_ROAD:
+      cost_name = "road";
+      if (c->ny < 2) throw RuntimeError{"road cost needs at least 2 output channels"};
+      if (!((float)pc(p, 0, 1.0) > 0.0f)) throw RuntimeError{"road cost: half_width must be > 0"};
+      break;
+    case SMPC_COST_CIRCLE_TRACK: {
+      cost_name = "circle_track";
+      const float in = (float)pc(p, 0, 1.875), out = (float)pc(p, 1, 2.125);
+      if (!(in > 0.0f) || !(in < out)) throw RuntimeError{"circle_track cost: need 0 < inner_radius < outer_radius"};
+      cost_ny = 4, cost_nu = 2;
+      break;
+    }
+    case SMPC_COST_DIFF_DRIVE_NAV:
+      cost_name = "diff_drive_nav";
+      cost_ny = 3, cost_nu = 2;
+      if (!(p.costmap_resolution > 0.0)) throw RuntimeError{"costmap: resolution must be > 0"};
+      if (p.costmap_cells_x < 1 || p.costmap_cells_y < 1) throw RuntimeError{"costmap: dimensions give an empty grid"};
+      break;
+    case SMPC_COST_QUADRATIC:
+      cost_name = "quadratic";
+      if (p.n_quad < 1 || p.n_quad > SMPC_MAX_DIM)
+        throw RuntimeError{"quadratic cost: target and weights must be non-empty and equal length"};
+      for (int i = 0; i < p.n_quad; ++i)
+        if (!(p.quad_weights[i] >= 0.0f)) throw RuntimeError{"quadratic cost: weights must be >= 0"};
+      cost_ny = p.n_quad;
+      break;
+    default: throw ConfigError{"cost.kind is not recognized"};
+  }
+  static const char* dyn_names[] = {"unicycle", "cartpole", "diff_drive", "double_integrator"};
+  if (cost_ny != c->ny)
+    throw ConfigError{"cost '" + cost_name + "' expects " + std::to_string(cost_ny) +
+                      " output channels but model '" + dyn_names[p.dynamics_kind] + "' produces " +
+                      std::to_string(c->ny)};
+  if (cost_nu != c->nu) throw RuntimeError{"rollout request cost dimensions do not match the model"};
+  // sampler
+  if (p.n_control_std == 1 && c->nu > 1) {
+  } else if (p.n_control_std != c->nu) {
+    throw RuntimeError{"sampler: std_dev needs one entry per control channel"};
+  }
+  for (int i = 0; i < p.n_control_std; ++i)
+    if (!(p.control_std[i] > 0.0f)) throw RuntimeError{"sampler: std_dev entries must be > 0"};
+  if (p.std_per_step) {
+    for (int i = 0; i < p.horizon * c->nu; ++i)
+      if (!(p.std_per_step[i] > 0.0f)) throw RuntimeError{"sampler: std_per_step entries must be > 0"};
+  }
+  if (!(p.zero_mean_fraction >= 0.0 && p.zero_mean_fraction <= 1.0))
+    throw RuntimeError{"sampler: zero_mean_fraction must be in [0, 1]"};
+  // controller
+  if (p.num_samples < 1) throw RuntimeError{name + ": num_samples must be >= 1"};
+  if (p.iterations < 1 || p.iterations > 256) throw RuntimeError{name + ": iterations must be in [1, 256]"};
+  if (!(p.lambda > 0.0)) throw RuntimeError{name + ": lambda must be > 0"};
+  if (!(p.dt > 0.0)) throw RuntimeError{name + ": dt must be > 0"};
+  if (p.horizon < 1) throw RuntimeError{name + ": horizon must be >= 1"};
+  if (!(p.n_step_sizes == 0 || p.n_step_sizes == 1 || p.n_step_sizes == p.horizon))
+    throw RuntimeError{name + ": step_sizes must be empty, scalar, or one per timestep"};
+  for (int i = 0; i < p.n_step_sizes; ++i)
+    if (!(p.step_sizes[i] > 0.0f && p.step_sizes[i] <= 1.0f))
+      throw RuntimeError{name + ": step sizes must be in (0, 1]"};
+  if (p.controller_kind == SMPC_CTRL_TUBE && !(p.nominal_reset_bound > 0.0))
+    throw RuntimeError{"tube: nominal_reset_bound must be > 0"};
+  if (p.horizon > (1 << 22)) throw RuntimeError{name + ": horizon too large"};
+  if (c->nx > kMaxNX || c->nu > kMaxNU || c->ny > kMaxNY) throw RuntimeError{"ModelDims: dimension exceeds capacity"};
+}
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+void fill_args(smpc_ctx* c) {
+  IterArgs& a = c->base;
+  const smpc_problem& p = c->p;
+  a.T = c->T;
+  a.S = c->S;
+  a.M_local = (int)c->M_local;
+  a.m_begin = c->m_begin;
+  a.M_global = c->M;
+  a.dt = (float)p.dt;  // engine.cpp:136, :216
+  a.lambda = p.lambda;
+  a.key0 = (uint32_t)p.seed;
+  a.key1 = (uint32_t)(p.seed >> 32);
+  a.with_mean = p.include_mean_sample != 0;
+  // zero-mean quota filled from the tail (sampling.cpp:56-62)
+  long long n_zero = (long long)ceil(p.zero_mean_fraction * (double)c->M);
+  n_zero = std::min(n_zero, a.with_mean ? c->M - 1 : c->M);
+  a.zero_begin = c->M - n_zero;
+  a.importance = p.importance_sampling != 0;
+  a.world = c->world;
+  a.rank = c->rank;
+  a.solve_count = &c->header()->solve_count;
+  a.iter = 0;
+  a.stream = 0;
+  a.mean_in = c->d_mean;
+  a.mean_out = c->d_mean;
+  a.x0 = c->d_x0;
+  a.sigma = c->d_sigma;
+  a.sig2 = c->d_sig2;
+  a.gamma = c->d_gamma;
+  a.eps_in = nullptr;
+  a.tail = c->d_tail;
+  a.costs = c->d_costs;
+  a.outputs = nullptr;
+  a.n_roll_blocks = c->n_roll_blocks;
+  a.blk_min = c->d_blk_min;
+  a.blk_arg = c->d_blk_arg;
+  a.counters = c->d_counters;
+  a.gather1 = c->d_gather1;
+  a.weights = c->d_weights;
+  a.n_w_blocks = c->n_w_blocks;
+  a.blk_eta = c->d_blk_eta;
+  a.blk_nz = c->d_blk_nz;
+  a.gather2 = c->d_gather2;
+  a.n_u_blocks = c->n_u_blocks;
+  a.blk_part = c->d_blk_part;
+  a.gather3 = c->d_gather3;
+  a.header = c->header();
+  a.controls = reinterpret_cast<float*>(c->d_result + c->off_controls);
+  a.states = reinterpret_cast<float*>(c->d_result + c->off_states);
+  a.outs_nom = reinterpret_cast<float*>(c->d_result + c->off_outs);
+  a.do_finish = 0;
+  a.normalize_weights = 0;
+  for (int i = 0; i < 8; ++i) a.dyn.p[i] = 0.f;
+  switch (p.dynamics_kind) {
+    case SMPC_DYN_CARTPOLE:
+      a.dyn.p[0] = (float)pd(p, 0, 1.0), a.dyn.p[1] = (float)pd(p, 1, 1.0);
+      a.dyn.p[2] = (float)pd(p, 2, 1.0), a.dyn.p[3] = (float)pd(p, 3, 9.81);
+      break;
+    case SMPC_DYN_DIFF_DRIVE: {
+      const double d[6] = {1.0, 1.0, -0.35, 0.5, -0.5, 0.5};
+      for (int i = 0; i < 6; ++i) a.dyn.p[i] = (float)pd(p, i, d[i]);
+      break;
+    }
+    default: break;
+  }
+  CostParams& cp = a.cost;
+  memset(&cp, 0, sizeof(cp));
+  switch (p.cost_kind) {
+    case SMPC_COST_ROAD: {
+      const double d[3] = {1.0, 1.0, 10.0};
+      for (int i = 0; i < 3; ++i) cp.p[i] = (float)pc(p, i, d[i]);
+      break;
+    }
+    case SMPC_COST_CIRCLE_TRACK: {
+      const double d[7] = {1.875, 2.125, 1000.0, 2.0, 2.0, 4.0, 2.0};
+      for (int i = 0; i < 7; ++i) cp.p[i] = (float)pc(p, i, d[i]);
+      break;
+    }
+    case SMPC_COST_DIFF_DRIVE_NAV: {
+      const double d[6] = {2.0, 2.0, 0.0, 5.0, 5.0, 20.0};
+      for (int i = 0; i < 6; ++i) cp.p[i] = (float)pc(p, i, d[i]);
+      cp.grid = c->d_costmap;
+      cp.cells_x = p.costmap_cells_x;
+      cp.cells_y = p.costmap_cells_y;
+      cp.origin_x = (float)p.costmap_origin_x;
+      cp.origin_y = (float)p.costmap_origin_y;
+      cp.inv_resolution = (float)(1.0 / p.costmap_resolution);  // costmap.cpp:21
+      cp.map_in_smem = (size_t)cp.cells_x * cp.cells_y <= 96 * 1024;
+      break;
+    }
+    case SMPC_COST_QUADRATIC:
+      cp.n_quad = p.n_quad;
+      for (int i = 0; i < p.n_quad; ++i) cp.target[i] = p.quad_target[i], cp.weights[i] = p.quad_weights[i];
+      break;
+  }
+}
+
+// Number of entries of the Phi^-1 tail table (see philox_normal.cuh).
+uint32_t tail_table_size() {
+  const float kLow = 0.02425f;
+  const volatile float one = 1.0f;
+  const float kHigh = one - kLow;
+  uint32_t j_lo = 0, j_hi = 1u << 23;
+  for (uint32_t j = 0; j < (1u << 23); ++j) {
+    const float pj = (float)j * 0x1.0p-23f + 0x1.0p-24f;
+    if (pj < kLow) j_lo = j + 1;
+    if (pj > kHigh && j < j_hi) j_hi = j;
+  }
+  return std::max(j_lo, (1u << 23) - j_hi);
+}
+
+void decode_error(smpc_ctx* c, unsigned long long key) {
+  const unsigned stage = (unsigned)(key >> 62);
+  const long long m = (long long)((key >> 30) & 0x7fffffffULL);
+  const int t = (int)((key >> 6) & 0xffffff);
+  const unsigned phase = (unsigned)((key >> 4) & 3);
+  const int ch = (int)(key & 15);
+  char buf[256];
+  if (stage == 0 && phase == 0) {
+    snprintf(buf, sizeof buf, "rollout produced non-finite state channel %d at sample %lld timestep %d", ch, m, t);
+  } else if (stage == 0) {
+    snprintf(buf, sizeof buf, "rollout produced invalid running cost at sample %lld timestep %d", m, t);
+  } else if (stage == 1) {
+    snprintf(buf, sizeof buf, "compute_weights: non-finite cost at sample %lld", m);
+  } else if (phase == 1) {
+    snprintf(buf, sizeof buf, "control vector has non-finite entry at channel %d", ch);
+  } else {
+    snprintf(buf, sizeof buf, "state vector has non-finite entry at channel %d", ch);
+  }
+  c->err = buf;
+  c->err_sample = stage <= 1 ? m : -1;
+  c->err_t = stage == 0 ? t : -1;
+  c->err_ch = (stage == 0 && phase == 0) || stage == 2 ? ch : -1;
+}
+
+// One solve's device work on c->stream (graph-captured or direct).
+void enqueue_solve(smpc_ctx* c, bool timed) {
+  CK(launch_begin_solve(c->header(), c->stream));
+  for (int it = 0; it < c->I; ++it) {
+    IterArgs a = c->base;
+    a.iter = it;
+    a.do_finish = it == c->I - 1;
+    if (timed) CK(cudaEventRecord(c->ev[2 * it], c->stream));
+    CK(c->ops.rollout(a, c->p.cost_kind, c->stream));
+    if (timed) CK(cudaEventRecord(c->ev[2 * it + 1], c->stream));
+    if (c->world > 1) {
+      const size_t n1 = (size_t)c->S * 2;
+      if (nccl()->AllGather(c->d_gather1 + c->rank * n1, c->d_gather1, n1, ncclFloat64, c->comm, c->stream))
+        throw CudaError{"ncclAllGather (rho) failed"};
+    }
+    CK(c->ops.weights(a, c->stream));
+    if (c->world > 1) {
+      const size_t n2 = (size_t)c->S * 2;
+      if (nccl()->AllGather(c->d_gather2 + c->rank * n2, c->d_gather2, n2, ncclFloat64, c->comm, c->stream))
+        throw CudaError{"ncclAllGather (eta) failed"};
+    }
+    CK(c->ops.update(a, c->stream));
+    if (c->world > 1) {
+      const size_t n3 = (size_t)c->S * c->T * c->nu;
+      if (nccl()->AllGather(c->d_gather3 + c->rank * n3, c->d_gather3, n3, ncclFloat64, c->comm, c->stream))
+        throw CudaError{"ncclAllGather (weighted sums) failed"};
+      CK(c->ops.combine(a, c->stream));
+    }
+  }
+  CK(launch_finish_solve(c->header(), c->stream));
+}
+
+void build_graph(smpc_ctx* c) {
+  if (c->graph) {
+    cudaGraphExecDestroy(c->graph);
+    c->graph = nullptr;
+  }
+  cudaGraph_t g;
+  CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+  try {
+    enqueue_solve(c, false);
+  } catch (...) {
+    cudaStreamEndCapture(c->stream, &g);
+    throw;
+  }
+  CK(cudaStreamEndCapture(c->stream, &g));
+  CK(cudaGraphInstantiate(&c->graph, g, 0));
+  cudaGraphDestroy(g);
+}
+
+void launch_solve(smpc_ctx* c) {
+  if (c->timing) {
+    enqueue_solve(c, true);
+  } else {
+    if (!c->graph) build_graph(c);
+    CK(cudaGraphLaunch(c->graph, c->stream));
+  }
+}
+
+void collect_timing(smpc_ctx* c) {
+  if (!c->timing) return;
+  for (int it = 0; it < c->I; ++it) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, c->ev[2 * it], c->ev[2 * it + 1]));
+    c->rollout_ms_total += ms;
+    c->rollout_launches += 1;
+  }
+}
+
+// Copies the result region back and checks the error key.
+void fetch_results(smpc_ctx* c) {
+  CK(cudaMemcpyAsync(c->h_result, c->d_result, c->result_bytes, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  collect_timing(c);
+  const ResultHeader* h = c->h_header();
+  if (h->err_key != kNoError) {
+    decode_error(c, h->err_key);
+    throw RuntimeError{c->err};
+  }
+  c->solve_count = h->solve_count;
+}
+
+void upload_x0(smpc_ctx* c, const float* x0, int S) {
+  memcpy(c->h_x0, x0, sizeof(float) * S * c->nx);
+  CK(cudaMemcpyAsync(c->d_x0, c->h_x0, sizeof(float) * S * c->nx, cudaMemcpyHostToDevice, c->stream));
+}
+
+void copy_solution(smpc_ctx* c, int s, smpc_solution* out) {
+  const ResultHeader* h = c->h_header();
+  const float* controls = reinterpret_cast<const float*>(c->h_result + c->off_controls);
+  const float* states = reinterpret_cast<const float*>(c->h_result + c->off_states);
+  const float* outs = reinterpret_cast<const float*>(c->h_result + c->off_outs);
+  const size_t TU = (size_t)c->T * c->nu;
+  if (out->controls) memcpy(out->controls, controls + s * TU, sizeof(float) * TU);
+  if (out->states) memcpy(out->states, states + (size_t)s * (c->T + 1) * c->nx, sizeof(float) * (c->T + 1) * c->nx);
+  if (out->outputs) memcpy(out->outputs, outs + (size_t)s * c->T * c->ny, sizeof(float) * c->T * c->ny);
+  out->summary.baseline = h->rho[s];
+  out->summary.normalizer = h->eta[s];
+  out->summary.argmin = h->argmin[s];
+  out->summary.nonzero = h->nonzero[s];
+}
+
+void fetch_weights(smpc_ctx* c, int s, double* dst) {
+  IterArgs a = c->base;
+  CK(launch_normalize_weights(a, c->stream));
+  CK(cudaMemcpyAsync(dst, c->d_weights + (size_t)s * c->M_local, sizeof(double) * c->M_local,
+                     cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+}
+
+double now_ms() {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+}  // namespace
+
+// ============================================================================
+extern "C" {
+
+const char* smpc_version(void) { return "paper_2409_07563_b200 0.1 (sm_100a)"; }
+
+smpc_status smpc_create(const smpc_problem* problem, smpc_ctx** out) {
+  if (!problem || !out) return SMPC_ERR_ARGUMENT;
+  *out = nullptr;
+  smpc_ctx* c = new smpc_ctx();
+  c->p = *problem;
+  c->fma = smpc_host_libm_uses_fma() != 0;
+  const smpc_status st = guarded(nullptr, [&] {
+    validate(c);
+    smpc_problem& p = c->p;
+    c->T = p.horizon;
+    c->I = p.iterations;
+    c->M = p.num_samples;
+    c->S = p.controller_kind == SMPC_CTRL_TUBE ? 2 : 1;
+    c->m_begin = 0;
+    long long m_end = c->M;
+    if (p.shard_end > 0) {
+      if (p.shard_begin < 0 || p.shard_end > c->M || p.shard_begin >= p.shard_end)
+        throw ConfigError{"smpc_problem: invalid shard range"};
+      c->m_begin = p.shard_begin;
+      m_end = p.shard_end;
+    }
+    c->M_local = m_end - c->m_begin;
+    const int TU = c->T * c->nu;
+    // own copies of borrowed arrays
+    if (p.std_per_step) c->std_per_step.assign(p.std_per_step, p.std_per_step + TU);
+    if (p.n_step_sizes > 0) c->step_sizes.assign(p.step_sizes, p.step_sizes + p.n_step_sizes);
+    if (p.costmap) c->costmap.assign(p.costmap, p.costmap + (size_t)p.costmap_cells_x * p.costmap_cells_y);
+    p.std_per_step = nullptr;
+    p.step_sizes = nullptr;
+    p.costmap = nullptr;
+
+    CK(cudaSetDevice(p.device));
+    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    c->n_roll_blocks = (int)((c->M_local + kRolloutThreads - 1) / kRolloutThreads);
+    c->n_w_blocks = (int)std::min<long long>((c->M_local + 255) / 256, 148 * 4);
+    c->n_u_blocks = (int)std::max<long long>(1, std::min<long long>((c->M_local + 255) / 256, 148 * 4));
+
+    c->d_mean = dalloc<float>((size_t)c->S * TU);
+    c->d_x0 = dalloc<float>((size_t)2 * kMaxNX);
+    c->d_sigma = dalloc<float>(TU);
+    c->d_sig2 = dalloc<double>(TU);
+    c->d_gamma = dalloc<double>(c->T);
+    c->d_costs = dalloc<double>((size_t)c->S * c->M_local);
+    c->d_weights = dalloc<double>((size_t)c->S * c->M_local);
+    c->d_blk_min = dalloc<double>((size_t)c->S * c->n_roll_blocks);
+    c->d_blk_arg = dalloc<long long>((size_t)c->S * c->n_roll_blocks);
+    c->d_blk_eta = dalloc<double>((size_t)c->S * c->n_w_blocks);
+    c->d_blk_nz = dalloc<long long>((size_t)c->S * c->n_w_blocks);
+    c->d_blk_part = dalloc<double>((size_t)c->S * c->n_u_blocks * TU);
+    c->d_counters = dalloc<unsigned int>(16);
+    c->d_gather1 = dalloc<double>((size_t)c->S * 2 * 8);
+    c->d_gather2 = dalloc<double>((size_t)c->S * 2 * 8);
+    c->d_gather3 = dalloc<double>((size_t)c->S * TU * 8);
+    // result region: header | controls | states | outputs
+    size_t off = align_up(sizeof(ResultHeader), 256);
+    c->off_controls = off;
+    off = align_up(off + sizeof(float) * c->S * TU, 256);
+    c->off_states = off;
+    off = align_up(off + sizeof(float) * c->S * (c->T + 1) * c->nx, 256);
+    c->off_outs = off;
+    off = align_up(off + sizeof(float) * c->S * c->T * c->ny, 256);
+    c->result_bytes = off;
+    c->d_result = dalloc<unsigned char>(off);
+    CK(cudaMallocHost(&c->h_result, off));
+    CK(cudaMallocHost(&c->h_x0, sizeof(float) * 2 * kMaxNX));
+    {
+      ResultHeader h;
+      memset(&h, 0, sizeof h);
+      h.err_key = kNoError;
+      h.abort_key = kNoError;
+      CK(cudaMemcpy(c->d_result, &h, sizeof h, cudaMemcpyHostToDevice));
+    }
+    // sigma / sigma^2 (sampling.hpp:56-60, sampling.cpp:123) and gamma (engine.cpp:397-401)
+    std::vector<float> sig(TU);
+    std::vector<double> sig2(TU), gam(c->T);
+    for (int t = 0; t < c->T; ++t)
+      for (int u = 0; u < c->nu; ++u) {
+        const float s = !c->std_per_step.empty() ? c->std_per_step[t * c->nu + u]
+                                                 : (p.n_control_std == 1 ? p.control_std[0] : p.control_std[u]);
+        sig[t * c->nu + u] = s;
+        const double sd = s;
+        sig2[t * c->nu + u] = sd * sd;
+      }
+    for (int t = 0; t < c->T; ++t)
+      gam[t] = c->step_sizes.empty() ? 1.0 : (double)c->step_sizes[c->step_sizes.size() == 1 ? 0 : t];
+    CK(cudaMemcpy(c->d_sigma, sig.data(), sizeof(float) * TU, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->d_sig2, sig2.data(), sizeof(double) * TU, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->d_gamma, gam.data(), sizeof(double) * c->T, cudaMemcpyHostToDevice));
+    if (p.cost_kind == SMPC_COST_DIFF_DRIVE_NAV) {
+      const size_t cells = (size_t)p.costmap_cells_x * p.costmap_cells_y;
+      c->d_costmap = dalloc<uint8_t>(cells);
+      if (!c->costmap.empty()) CK(cudaMemcpy(c->d_costmap, c->costmap.data(), cells, cudaMemcpyHostToDevice));
+    }
+    const uint32_t n_tab = tail_table_size();
+    c->d_tail = dalloc<float>(n_tab);
+    CK(build_tail_table(c->d_tail, n_tab, c->stream));
+    c->host_mean[0].assign(TU, 0.f);
+    c->host_mean[1].assign(TU, 0.f);
+    c->nominal_state.assign(c->nx, 0.f);
+    for (int i = 0; i < 2 * c->I; ++i) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      c->ev.push_back(e);
+    }
+    fill_args(c);
+    CK(cudaStreamSynchronize(c->stream));
+  });
+  if (st != SMPC_OK) {
+    smpc_destroy(c);
+    return st;
+  }
+  *out = c;
+  return SMPC_OK;
+}
+
+void smpc_destroy(smpc_ctx* c) {
+  if (!c) return;
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->graph) cudaGraphExecDestroy(c->graph);
+  for (auto e : c->ev) cudaEventDestroy(e);
+  if (c->comm && nccl()) nccl()->CommDestroy(c->comm);
+  void* ptrs[] = {c->d_mean, c->d_x0, c->d_sigma, c->d_tail, c->d_sig2, c->d_gamma, c->d_costs,
+                  c->d_weights, c->d_blk_min, c->d_blk_eta, c->d_blk_part, c->d_gather1, c->d_gather2,
+                  c->d_gather3, c->d_blk_arg, c->d_blk_nz, c->d_counters, c->d_costmap, c->d_result,
+                  c->d_ro_x0, c->d_ro_mean, c->d_eps, c->d_outputs, c->d_wscratch, c->d_flags};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (c->h_result) cudaFreeHost(c->h_result);
+  if (c->h_x0) cudaFreeHost(c->h_x0);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+const char* smpc_last_error(const smpc_ctx* c) { return c ? c->err.c_str() : g_create_error.c_str(); }
+
+smpc_status smpc_error_location(const smpc_ctx* c, int64_t* sample, int32_t* timestep, int32_t* channel) {
+  if (!c) return SMPC_ERR_ARGUMENT;
+  if (sample) *sample = c->err_sample;
+  if (timestep) *timestep = c->err_t;
+  if (channel) *channel = c->err_ch;
+  return SMPC_OK;
+}
+
+smpc_status smpc_get_dims(const smpc_ctx* c, int32_t* nx, int32_t* nu, int32_t* ny) {
+  if (!c) return SMPC_ERR_ARGUMENT;
+  if (nx) *nx = c->nx;
+  if (nu) *nu = c->nu;
+  if (ny) *ny = c->ny;
+  return SMPC_OK;
+}
+
+smpc_status smpc_set_mean(smpc_ctx* c, int32_t system, const float* mean) {
+  if (!c || !mean || system < 0 || system >= c->S) return SMPC_ERR_ARGUMENT;
+  return guarded(c, [&] {
+    const size_t TU = (size_t)c->T * c->nu;
+    for (size_t k = 0; k < TU; ++k)
+      if (!std::isfinite(mean[k])) throw RuntimeError{"control vector has non-finite entry at channel " + std::to_string(k % c->nu)};
+    CK(cudaMemcpyAsync(c->d_mean + system * TU, mean, sizeof(float) * TU, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+smpc_status smpc_get_mean(const smpc_ctx* cc, int32_t system, float* mean) {
+  smpc_ctx* c = const_cast<smpc_ctx*>(cc);
+  if (!c || !mean || system < 0 || system >= c->S) return SMPC_ERR_ARGUMENT;
+  return guarded(c, [&] {
+    const size_t TU = (size_t)c->T * c->nu;
+    CK(cudaMemcpyAsync(mean, c->d_mean + system * TU, sizeof(float) * TU, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+smpc_status smpc_get_solve_count(const smpc_ctx* c, uint64_t* n) {
+  if (!c || !n) return SMPC_ERR_ARGUMENT;
+  *n = c->solve_count;
+  return SMPC_OK;
+}
+
+smpc_status smpc_set_solve_count(smpc_ctx* c, uint64_t n) {
+  if (!c) return SMPC_ERR_ARGUMENT;
+  return guarded(c, [&] {
+    CK(cudaMemcpyAsync(&c->header()->solve_count, &n, sizeof n, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    c->solve_count = n;
+  });
+}
+
+smpc_status smpc_compute_control(smpc_ctx* c, const float* x0, smpc_solution* out) {
+  if (!c || !x0) return SMPC_ERR_ARGUMENT;
+  if (c->S != 1) {
+    // TubeMppiController::compute_control returns the nominal solution (controllers.cpp:281-283).
+    smpc_tube_solution t{};
+    if (out) t.nominal = *out;
+    const smpc_status st = smpc_tube_compute_control(c, x0, &t);
+    if (out) *out = t.nominal;
+    return st;
+  }
+  return guarded(c, [&] {
+    const double t0 = now_ms();
+    for (int i = 0; i < c->nx; ++i)
+      if (!std::isfinite(x0[i])) throw RuntimeError{"state vector has non-finite entry at channel " + std::to_string(i)};
+    upload_x0(c, x0, 1);
+    launch_solve(c);
+    fetch_results(c);
+    if (out) {
+      copy_solution(c, 0, out);
+      if (out->weights) fetch_weights(c, 0, out->weights);
+      out->solve_time_ms = now_ms() - t0;
+    }
+  });
+}
+
+smpc_status smpc_tube_compute_control(smpc_ctx* c, const float* x_real, smpc_tube_solution* out) {
+  if (!c || !x_real) return SMPC_ERR_ARGUMENT;
+  if (c->S != 2) {
+    set_error(c, "tube_compute_control: context is not a tube controller");
+    return SMPC_ERR_RUNTIME;
+  }
+  return guarded(c, [&] {
+    const double t0 = now_ms();
+    for (int i = 0; i < c->nx; ++i)
+      if (!std::isfinite(x_real[i])) throw RuntimeError{"state vector has non-finite entry at channel " + std::to_string(i)};
+    // nominal-state bookkeeping (controllers.cpp:221-227)
+    if (!c->nominal_started) {
+      c->nominal_state.assign(x_real, x_real + c->nx);
+      c->nominal_started = true;
+    } else if (std::isfinite(c->p.nominal_reset_bound)) {
+      float acc = 0.f;
+      for (int i = 0; i < c->nx; ++i) {
+        const float d = x_real[i] - c->nominal_state[i];
+        acc += d * d;
+      }
+      if ((double)std::sqrt(acc) > c->p.nominal_reset_bound) c->nominal_state.assign(x_real, x_real + c->nx);
+    }
+    float x0s[2 * kMaxNX];
+    memcpy(x0s, c->nominal_state.data(), sizeof(float) * c->nx);
+    memcpy(x0s + c->nx, x_real, sizeof(float) * c->nx);
+    upload_x0(c, x0s, 2);
+    launch_solve(c);
+    fetch_results(c);
+    const double elapsed = now_ms() - t0;
+    if (out) {
+      if (out->nominal_state) memcpy(out->nominal_state, c->nominal_state.data(), sizeof(float) * c->nx);
+      copy_solution(c, 0, &out->nominal);
+      copy_solution(c, 1, &out->real);
+      if (out->nominal.weights) fetch_weights(c, 0, out->nominal.weights);
+      if (out->real.weights) fetch_weights(c, 1, out->real.weights);
+      out->nominal.solve_time_ms = elapsed;
+      out->real.solve_time_ms = elapsed;
+    }
+    // the nominal system advances only through the model (controllers.cpp:276-277)
+    const float* nn = c->h_header()->next_nominal_state;
+    c->nominal_state.assign(nn, nn + c->nx);
+  });
+}
+
+smpc_status smpc_shift_control_sequence(smpc_ctx* c, double elapsed_s, double dt_min) {
+  if (!c) return SMPC_ERR_ARGUMENT;
+  return guarded(c, [&] {
+    const std::string name = controller_name(c->p.controller_kind);
+    if (!(dt_min > 0.0)) throw RuntimeError{name + ": dt_min must be > 0"};
+    if (elapsed_s <= 0.0) return;
+    // controllers.cpp:68-84 (Tube shifts both means, :285-292)
+    const double quantized = (double)std::llrint(elapsed_s / dt_min) * dt_min;
+    const long long steps = std::llrint(quantized / c->p.dt);
+    if (steps <= 0) return;
+    const int T = c->T, nu = c->nu;
+    std::vector<float> m((size_t)T * nu), shifted((size_t)T * nu);
+    for (int s = 0; s < c->S; ++s) {
+      CK(cudaMemcpy(m.data(), c->d_mean + (size_t)s * T * nu, sizeof(float) * T * nu, cudaMemcpyDeviceToHost));
+      if (steps >= T) {
+        std::fill(shifted.begin(), shifted.end(), 0.f);
+      } else {
+        for (int t = 0; t < T; ++t) {
+          const int src = std::min<long long>(t + steps, T - 1);
+          for (int u = 0; u < nu; ++u) shifted[t * nu + u] = m[src * nu + u];
+        }
+      }
+      CK(cudaMemcpy(c->d_mean + (size_t)s * T * nu, shifted.data(), sizeof(float) * T * nu, cudaMemcpyHostToDevice));
+    }
+  });
+}
+
+smpc_status smpc_generate_samples(smpc_ctx* c, const float* mean, uint32_t stream, float* eps_out,
+                                  uint8_t* flags_out) {
+  if (!c || !mean || !eps_out) return SMPC_ERR_ARGUMENT;
+  return guarded(c, [&] {
+    const size_t TU = (size_t)c->T * c->nu;
+    const size_t n = (size_t)c->M_local * TU;
+    if (c->eps_cap < n) {
+      if (c->d_eps) cudaFree(c->d_eps);
+      c->d_eps = dalloc<float>(n);
+      c->eps_cap = n;
+    }
+    if (c->flags_cap < (size_t)c->M_local) {
+      if (c->d_flags) cudaFree(c->d_flags);
+      c->d_flags = dalloc<uint8_t>(c->M_local);
+      c->flags_cap = c->M_local;
+    }
+    if (!c->d_ro_mean) c->d_ro_mean = dalloc<float>(2 * TU);
+    CK(cudaMemcpyAsync(c->d_ro_mean, mean, sizeof(float) * TU, cudaMemcpyHostToDevice, c->stream));
+    IterArgs a = c->base;
+    a.solve_count = nullptr;
+    a.stream = stream;
+    a.mean_in = c->d_ro_mean;
+    CK(c->ops.generate(a, c->d_eps, c->d_flags, c->stream));
+    CK(cudaMemcpyAsync(eps_out, c->d_eps, sizeof(float) * n, cudaMemcpyDeviceToHost, c->stream));
+    if (flags_out) CK(cudaMemcpyAsync(flags_out, c->d_flags, c->M_local, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+smpc_status smpc_rollout(smpc_ctx* c, int32_t S, const float* x0s, const float* means, const float* eps,
+                         uint32_t stream, double* costs_out, float* outputs_out) {
+  if (!c || !x0s || !means || !costs_out || (S != 1 && S != 2)) return SMPC_ERR_ARGUMENT;
+  return guarded(c, [&] {
+    const size_t TU = (size_t)c->T * c->nu;
+    if (!c->d_ro_mean) c->d_ro_mean = dalloc<float>(2 * TU);
+    if (!c->d_ro_x0) c->d_ro_x0 = dalloc<float>(2 * kMaxNX);
+    CK(cudaMemcpyAsync(c->d_ro_mean, means, sizeof(float) * S * TU, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->d_ro_x0, x0s, sizeof(float) * S * c->nx, cudaMemcpyHostToDevice, c->stream));
+    IterArgs a = c->base;
+    a.S = S;
+    a.solve_count = nullptr;
+    a.stream = stream;
+    a.iter = 0;
+    a.mean_in = c->d_ro_mean;
+    a.x0 = c->d_ro_x0;
+    if (S > c->S) {  // scratch sized for the controller's S; grow for a 2-system request
+      if (!c->d_wscratch || c->wscratch_cap < (size_t)2 * c->M_local) {
+        if (c->d_wscratch) cudaFree(c->d_wscratch);
+        c->wscratch_cap = (size_t)2 * c->M_local + 2 * (size_t)c->n_roll_blocks;
+        c->d_wscratch = dalloc<double>(c->wscratch_cap);
+      }
+    }
+    double* costs = S > c->S ? c->d_wscratch : c->d_costs;
+    a.costs = costs;
+    // blk_min/arg and gather1 must hold S systems
+    double* blk_min = c->d_blk_min;
+    long long* blk_arg = c->d_blk_arg;
+    if (S > c->S) {
+      blk_min = dalloc<double>((size_t)2 * c->n_roll_blocks);
+      blk_arg = dalloc<long long>((size_t)2 * c->n_roll_blocks);
+    }
+    a.blk_min = blk_min;
+    a.blk_arg = blk_arg;
+    a.rank = 0;
+    a.world = 1;
+    if (eps) {
+      const size_t n = (size_t)c->M_local * TU;
+      if (c->eps_cap < n) {
+        if (c->d_eps) cudaFree(c->d_eps);
+        c->d_eps = dalloc<float>(n);
+        c->eps_cap = n;
+      }
+      CK(cudaMemcpyAsync(c->d_eps, eps, sizeof(float) * n, cudaMemcpyHostToDevice, c->stream));
+      a.eps_in = c->d_eps;
+    }
+    if (outputs_out) {
+      const size_t n = (size_t)S * c->M_local * c->T * c->ny;
+      if (c->outputs_cap < n) {
+        if (c->d_outputs) cudaFree(c->d_outputs);
+        c->d_outputs = dalloc<float>(n);
+        c->outputs_cap = n;
+      }
+      a.outputs = c->d_outputs;
+    }
+    // the kernel's abort gate reads the header: clear a previous failure first
+    CK(launch_begin_solve(c->header(), c->stream));
+    CK(c->ops.rollout(a, c->p.cost_kind, c->stream));
+    ResultHeader h;
+    CK(cudaMemcpyAsync(costs_out, costs, sizeof(double) * S * c->M_local, cudaMemcpyDeviceToHost, c->stream));
+    if (outputs_out)
+      CK(cudaMemcpyAsync(outputs_out, c->d_outputs, sizeof(float) * S * c->M_local * c->T * c->ny,
+                         cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(&h, c->header(), sizeof h, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (S > c->S) {
+      cudaFree(blk_min);
+      cudaFree(blk_arg);
+    }
+    if (h.err_key != kNoError && (h.err_key >> 62) == 0) {
+      decode_error(c, h.err_key);
+      throw RuntimeError{c->err};
+    }
+  });
+}
+
+smpc_status smpc_compute_weights(smpc_ctx* c, const double* costs, int64_t count, double lambda,
+                                 double* weights_out, smpc_weight_summary* summary) {
+  if (!c || !costs || count < 0) return SMPC_ERR_ARGUMENT;
+  return guarded(c, [&] {
+    if (!(lambda > 0.0)) throw RuntimeError{"compute_weights: lambda must be > 0"};
+    if (count == 0) throw RuntimeError{"compute_weights: cost list is empty"};
+    for (int64_t m = 0; m < count; ++m)
+      if (!std::isfinite(costs[m])) throw RuntimeError{"compute_weights: non-finite cost at sample " + std::to_string(m)};
+    const int nblk = (int)std::min<long long>((count + 255) / 256, 148 * 4);
+    const size_t need = (size_t)2 * count + 4 * (size_t)nblk + 8;
+    if (c->wscratch_cap < need) {
+      if (c->d_wscratch) cudaFree(c->d_wscratch);
+      c->d_wscratch = dalloc<double>(need);
+      c->wscratch_cap = need;
+    }
+    double* d_costs = c->d_wscratch;
+    double* d_w = d_costs + count;
+    double* d_bmin = d_w + count;
+    long long* d_barg = reinterpret_cast<long long*>(d_bmin + nblk);
+    double* d_eta = reinterpret_cast<double*>(d_barg + nblk);
+    double* d_nz = d_eta + nblk;
+    double* d_g1 = d_nz + nblk;  // [2]
+    double* d_g2 = d_g1 + 2;     // [2]
+    CK(cudaMemcpyAsync(d_costs, costs, sizeof(double) * count, cudaMemcpyHostToDevice, c->stream));
+    CK(launch_begin_solve(c->header(), c->stream));
+    CK(launch_min_only(d_costs, count, d_bmin, d_barg, nblk, c->d_counters + 8, d_g1,
+                       reinterpret_cast<long long*>(d_g1 + 1), c->stream));
+    IterArgs a = c->base;
+    a.S = 1;
+    a.world = 1;
+    a.rank = 0;
+    a.M_local = (int)count;
+    a.costs = d_costs;
+    a.weights = d_w;
+    a.lambda = lambda;
+    a.gather1 = d_g1;
+    a.gather2 = d_g2;
+    a.n_w_blocks = nblk;
+    a.blk_eta = d_eta;
+    a.blk_nz = reinterpret_cast<long long*>(d_nz);
+    CK(launch_weights(a, c->stream));
+    CK(launch_normalize_weights(a, c->stream));
+    double g1[2], g2[2];
+    if (weights_out) CK(cudaMemcpyAsync(weights_out, d_w, sizeof(double) * count, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(g1, d_g1, sizeof g1, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(g2, d_g2, sizeof g2, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (summary) {
+      summary->baseline = g1[0];
+      long long am;
+      memcpy(&am, &g1[1], sizeof am);
+      summary->argmin = am;
+      summary->normalizer = g2[0];
+      summary->nonzero = (int64_t)g2[1];
+    }
+  });
+}
+
+smpc_status smpc_set_x0(smpc_ctx* c, const float* x0) {
+  if (!c || !x0) return SMPC_ERR_ARGUMENT;
+  return guarded(c, [&] {
+    upload_x0(c, x0, c->S);
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+smpc_status smpc_launch_iteration(smpc_ctx* c) {
+  if (!c) return SMPC_ERR_ARGUMENT;
+  return guarded(c, [&] { launch_solve(c); });
+}
+
+smpc_status smpc_synchronize(smpc_ctx* c) {
+  if (!c) return SMPC_ERR_ARGUMENT;
+  return guarded(c, [&] {
+    CK(cudaMemcpyAsync(c->h_result, c->d_result, sizeof(ResultHeader), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    collect_timing(c);
+    const ResultHeader* h = c->h_header();
+    if (h->err_key != kNoError) {
+      decode_error(c, h->err_key);
+      throw RuntimeError{c->err};
+    }
+    c->solve_count = h->solve_count;
+  });
+}
+
+void* smpc_stream(smpc_ctx* c) { return c ? (void*)c->stream : nullptr; }
+
+int32_t smpc_kernels_per_solve(const smpc_ctx* c) {
+  if (!c) return 0;
+  return 2 + c->I * (3 + (c->world > 1 ? 1 : 0));
+}
+
+smpc_status smpc_rollout_kernel_ms(smpc_ctx* c, int32_t enable, double* total_ms, int64_t* launches) {
+  if (!c) return SMPC_ERR_ARGUMENT;
+  if (total_ms) *total_ms = c->rollout_ms_total;
+  if (launches) *launches = c->rollout_launches;
+  if (enable >= 0) {
+    c->timing = enable != 0;
+    c->rollout_ms_total = 0.0;
+    c->rollout_launches = 0;
+  }
+  return SMPC_OK;
+}
+
+smpc_status smpc_comm_unique_id(uint8_t id_out[128]) {
+  NcclApi* api = nccl();
+  if (!api) {
+    g_create_error = "NCCL (libnccl.so.2) could not be loaded";
+    return SMPC_ERR_CUDA;
+  }
+  ncclUniqueId id;
+  if (api->GetUniqueId(&id) != 0) return SMPC_ERR_CUDA;
+  memcpy(id_out, id.internal, 128);
+  return SMPC_OK;
+}
+
+smpc_status smpc_comm_init(smpc_ctx* c, const uint8_t id[128], int32_t rank, int32_t world) {
+  if (!c || !id || world < 1 || rank < 0 || rank >= world || world > 8) return SMPC_ERR_ARGUMENT;
+  return guarded(c, [&] {
+    if (world == 1) return;
+    NcclApi* api = nccl();
+    if (!api) throw CudaError{"NCCL (libnccl.so.2) could not be loaded"};
+    ncclUniqueId uid;
+    memcpy(uid.internal, id, 128);
+    CK(cudaSetDevice(c->p.device));
+    const ncclResult_t r = api->CommInitRank(&c->comm, world, uid, rank);
+    if (r != 0) throw CudaError{std::string("ncclCommInitRank: ") + (api->GetErrorString ? api->GetErrorString(r) : "")};
+    c->rank = rank;
+    c->world = world;
+    fill_args(c);
+    if (c->graph) {
+      cudaGraphExecDestroy(c->graph);
+      c->graph = nullptr;
+    }
+  });
+}
+
+}  // extern "C"
