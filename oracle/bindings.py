@@ -79,6 +79,12 @@ class Oracle:
             L.oracle_compute_control.argtypes = [ctypes.POINTER(SmpcProblem), _f32p, ctypes.POINTER(ctypes.c_uint64),
                                                  _f32p, _f32p, _f32p, _f32p, ctypes.c_void_p,
                                                  ctypes.POINTER(SmpcWeightSummary), ctypes.POINTER(_OracleErr)]
+            L.oracle_running_cost.argtypes = [ctypes.POINTER(SmpcProblem), _f32p]
+            L.oracle_running_cost.restype = ctypes.c_double
+            L.oracle_terminal_cost.argtypes = [ctypes.POINTER(SmpcProblem), _f32p]
+            L.oracle_terminal_cost.restype = ctypes.c_double
+            L.oracle_step.argtypes = [ctypes.POINTER(SmpcProblem), _f32p, _f32p, ctypes.c_float, _f32p, _f32p,
+                                      ctypes.POINTER(_OracleErr)]
             L.oracle_tube_compute_control.argtypes = [
                 ctypes.POINTER(SmpcProblem), _f32p, _f32p, _f32p, ctypes.POINTER(ctypes.c_int32),
                 ctypes.POINTER(ctypes.c_uint64), _f32p, _f32p, _f32p, _f32p, _f32p,
@@ -120,6 +126,26 @@ class Oracle:
         out = np.zeros(1 << 23, np.float32)
         self.lib.oracle_icdf_domain(out)
         return out
+
+    # ---- plugins ----------------------------------------------------------------
+    def running_cost(self, sc: Scenario, y) -> float:
+        p = sc.to_problem()
+        return self.lib.oracle_running_cost(ctypes.byref(p), np.ascontiguousarray(y, np.float32))
+
+    def terminal_cost(self, sc: Scenario, y) -> float:
+        p = sc.to_problem()
+        return self.lib.oracle_terminal_cost(ctypes.byref(p), np.ascontiguousarray(y, np.float32))
+
+    def step(self, sc: Scenario, x, u, dt: float):
+        n_x, n_u, n_y = sc.dims
+        p = sc.to_problem()
+        xn = np.zeros(n_x, np.float32)
+        y = np.zeros(n_y, np.float32)
+        err = _OracleErr()
+        rc = self.lib.oracle_step(ctypes.byref(p), np.ascontiguousarray(x, np.float32),
+                                  np.ascontiguousarray(u, np.float32), dt, xn, y, ctypes.byref(err))
+        self._check(rc, err.message)
+        return xn, y
 
     # ---- sampler / engine ----------------------------------------------------
     def generate_samples(self, sc: Scenario, mean: np.ndarray, stream: int, m_begin: int = 0,

@@ -1,0 +1,134 @@
+"""Generate tests/golden/*.npz from the UNMODIFIED reference (oracle/_ref).
+
+TEST INFRASTRUCTURE ONLY. Run here (where /root/reference exists):
+    python oracle/gen_golden.py
+Each fixture records, for one scenario: the reference's noise batch, rollout
+costs (fused and split strategies, 3 workers), stored trajectories, the
+compute_weights result, and three warm-started compute_control solves (or
+tube solves). The C restatement (oracle/smpc_oracle.c) and the GPU path are
+checked against these files; /root/reference is not needed at test time.
+"""
+import json
+import os
+import sys
+import zlib
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from oracle.bindings import Oracle, OracleController, build  # noqa: E402
+from paper_2409_07563_b200 import scenario as S  # noqa: E402
+
+OUT = os.path.join(ROOT, "tests", "golden")
+OBSTACLES = "/root/reference/proj/configs/obstacles.costmap"
+
+
+def fixture_scenarios():
+    sc = {}
+    sc["cartpole_c1"] = S.cartpole_scenario(num_samples=256, horizon=100, seed=1)
+    sc["di_swarm_c5"] = S.di_swarm_scenario(num_samples=512, horizon=100, seed=7)
+    nav = S.diff_drive_nav_scenario(num_samples=200, horizon=56, seed=42,
+                                    costmap=S.Costmap.load(OBSTACLES))
+    nav.control_std = (1.0, 1.0)  # proj/configs/diff_drive_nav.json uses sigma = 1
+    sc["diffdrive_nav_obstacles"] = nav
+    sc["diffdrive_nav_synthetic"] = S.diff_drive_nav_scenario(num_samples=200, horizon=56, seed=3)
+    sc["unicycle_road_zero_mean"] = S.Scenario(num_samples=160, horizon=40, dynamics="unicycle", cost="road",
+                                               rng_seed=11, control_std=(0.5, 0.3), zero_mean_fraction=0.25)
+    sc["cartpole_perstep_nomean"] = S.Scenario(num_samples=128, horizon=30, dynamics="cartpole", cost="road",
+                                               rng_seed=5, control_std=(1.0,),
+                                               std_per_step=[[0.5 + 0.02 * t] for t in range(30)],
+                                               zero_mean_fraction=0.1, include_mean_sample=False)
+    sc["di_quadratic_dmd"] = S.Scenario(num_samples=192, horizon=25, dynamics="double_integrator", cost="quadratic",
+                                        target=[1.0, -1.0, 0.0, 0.0], weights=[1.0, 1.0, 0.1, 0.1], rng_seed=3,
+                                        control_std=(0.7, 0.4), controller="dmd", step_size=0.6, lambda_=2.0)
+    circle = S.di_swarm_scenario(num_samples=256, horizon=32, seed=7)
+    circle.controller, circle.step_size = "dmd", 0.8  # proj/configs/circle_track_dmd.json
+    sc["circle_track_dmd_config"] = circle
+    tube = S.cartpole_scenario(num_samples=256, horizon=50, seed=4)
+    tube.controller = "tube"
+    sc["cartpole_tube"] = tube
+    return sc
+
+
+def scenario_record(sc: S.Scenario) -> dict:
+    d = {k: v for k, v in vars(sc).items() if k != "costmap"}
+    d["control_std"] = list(sc.control_std)
+    return d
+
+
+def main():
+    build()
+    R = Oracle("reference")
+    os.makedirs(OUT, exist_ok=True)
+    index = {}
+    for name, sc in fixture_scenarios().items():
+        n_x, n_u, n_y = sc.dims
+        T = sc.horizon
+        rng = np.random.default_rng(zlib.crc32(name.encode()))
+        mean = (rng.standard_normal((T, n_u)) * 0.2).astype(np.float32)
+        stream = 5
+        eps, flags = R.generate_samples(sc, mean, stream, workers=3)
+        S_ = 2 if sc.controller == "tube" else 1
+        means = np.stack([mean] + [mean * 0.5] * (S_ - 1)).astype(np.float32)
+        x0s = np.stack([sc.x0() + np.float32(0.05 * s) for s in range(S_)]).astype(np.float32)
+        costs_split, outputs = R.rollout(sc, x0s, means, eps, outputs=True, workers=3)
+        costs_fused = R.rollout(sc, x0s, means, eps, strategy=1, workers=3)
+        assert np.array_equal(costs_split, costs_fused)
+        w, rho, eta, am = R.compute_weights(costs_fused[0], sc.lambda_)
+        rec = dict(mean=mean, stream=np.int64(stream), eps=eps, flags=flags, x0s=x0s, means=means,
+                   costs=costs_fused, outputs=outputs, weights=w, rho=np.float64(rho), eta=np.float64(eta),
+                   argmin=np.int64(am))
+        ctl = OracleController(sc, "reference", workers=3)
+        x = sc.x0()
+        for k in range(3):
+            if sc.controller == "tube":
+                r = ctl.tube_compute_control(x)
+                rec[f"solve{k}_x"] = x.copy()
+                rec[f"solve{k}_nominal_controls"] = r["nominal_controls"]
+                rec[f"solve{k}_real_controls"] = r["real_controls"]
+                rec[f"solve{k}_nominal_states"] = r["nominal_states"]
+                rec[f"solve{k}_real_states"] = r["real_states"]
+                rec[f"solve{k}_nominal_state"] = r["nominal_state"]
+                for side in ("nominal", "real"):
+                    rec[f"solve{k}_{side}_rho"] = np.float64(r[side]["baseline"])
+                    rec[f"solve{k}_{side}_eta"] = np.float64(r[side]["normalizer"])
+                    rec[f"solve{k}_{side}_argmin"] = np.int64(r[side]["argmin"])
+                x = x + np.float32(0.01)
+            else:
+                r = ctl.compute_control(x, want_weights=True)
+                rec[f"solve{k}_controls"] = r["controls"]
+                rec[f"solve{k}_states"] = r["states"]
+                rec[f"solve{k}_outputs"] = r["outputs"]
+                rec[f"solve{k}_weights"] = r["weights"]
+                rec[f"solve{k}_rho"] = np.float64(r["baseline"])
+                rec[f"solve{k}_eta"] = np.float64(r["normalizer"])
+                rec[f"solve{k}_argmin"] = np.int64(r["argmin"])
+        cm = sc.effective_costmap()
+        if cm is not None:
+            rec["costmap"] = cm.grid
+            rec["costmap_geom"] = np.array([cm.resolution, cm.origin_x, cm.origin_y])
+        np.savez_compressed(os.path.join(OUT, f"{name}.npz"), **rec)
+        index[name] = scenario_record(sc)
+        print(name, "rho", rho, "argmin", am, "bytes", os.path.getsize(os.path.join(OUT, f"{name}.npz")))
+    # Random123 Philox4x32-10 known-answer vectors and reference normals.
+    kat = {
+        "philox": [
+            [[0, 0, 0, 0], [0, 0], [int(v) for v in R.philox([0, 0, 0, 0], [0, 0])]],
+            [[0xFFFFFFFF] * 4, [0xFFFFFFFF] * 2, [int(v) for v in R.philox([0xFFFFFFFF] * 4, [0xFFFFFFFF] * 2)]],
+            [[0x243F6A88, 0x85A308D3, 0x13198A2E, 0x03707344], [0xA4093822, 0x299F31D0],
+             [int(v) for v in R.philox([0x243F6A88, 0x85A308D3, 0x13198A2E, 0x03707344], [0xA4093822, 0x299F31D0])]],
+        ],
+        "quad": [[seed, a, b, c, [float(v).hex() for v in R.quad(seed, a, b, c)]]
+                 for seed, a, b, c in [(0, 0, 0, 0), (0, 0, 1, 0), (0, 0, 4, 0), (42, 0, 1, 0), (7, 256, 5221, 3)]],
+    }
+    with open(os.path.join(OUT, "index.json"), "w") as f:
+        json.dump({"scenarios": index, "kat": kat,
+                   "generator": "oracle/gen_golden.py via oracle/_ref/libsmpc_ref.so (reference compiled from "
+                                "/root/reference/proj/core/src with the Eigen-subset shim)"}, f, indent=1,
+                  default=lambda o: list(o) if isinstance(o, tuple) else o)
+
+
+if __name__ == "__main__":
+    main()

@@ -622,3 +622,7 @@ int oracle_tube_compute_control(const smpc_problem* p, float* nominal_mean, floa
   memcpy(nominal_state, xn, sizeof(float) * d.n_x);
   return 0;
 }
+
+/* CostFunction::running_cost_raw / terminal_cost_raw (costs.hpp:24-25) for unit tests. */
+double oracle_running_cost(const smpc_problem* p, const float* y) { return running_cost(p, y); }
+double oracle_terminal_cost(const smpc_problem* p, const float* y) { return terminal_cost(p, y); }

@@ -30,6 +30,16 @@ __host__ __device__ inline unsigned long long make_error_key(unsigned stage, uns
          ((unsigned long long)(phase & 3) << 4) | (unsigned long long)(ch & 15);
 }
 
+// Philox round keys (see philox_normal.cuh) and the runtime {1,1} / {-0,-0}
+// f32x2 operands that keep ptxas from contracting packed mul+add.
+struct PhiloxKeys {
+  uint32_t k0[10], k1[10];
+};
+struct PackConst {
+  unsigned long long one;    // {1.0f, 1.0f}
+  unsigned long long mzero;  // {-0.0f, -0.0f}
+};
+
 // Model / cost parameters as plain floats (device functors are built from these).
 struct DynParams {
   float p[8];
@@ -66,6 +76,9 @@ struct IterArgs {
   float dt;
   double lambda;
   uint32_t key0, key1;
+  PhiloxKeys rk;         // round keys of (key0, key1)
+  PackConst pk;
+  uint32_t j_lo, j_hi;   // uniform index j = w >> 9 is a lower tail iff j < j_lo, upper iff j >= j_hi
   int with_mean;
   long long zero_begin;
   int importance;
@@ -108,6 +121,7 @@ struct IterArgs {
   float* outs_nom;  // [S][T][NY]
   int do_finish;    // final iteration of a solve: nominal rollout + solve_count++
   int normalize_weights;  // write w = e/eta back (only when the caller wants weights)
+  double skip_w;          // update skips samples with w_m < skip_w (0 = exact)
   DynParams dyn;
   CostParams cost;
 };

@@ -279,11 +279,15 @@ void validate(smpc_ctx* c) {
       throw RuntimeError{name + ": step sizes must be in (0, 1]"};
   if (p.controller_kind == SMPC_CTRL_TUBE && !(p.nominal_reset_bound > 0.0))
     throw RuntimeError{"tube: nominal_reset_bound must be > 0"};
+  if (!(p.update_skip_mass >= 0.0 && p.update_skip_mass < 1e-6))
+    throw RuntimeError{name + ": update_skip_mass must be in [0, 1e-6)"};
   if (p.horizon > (1 << 22)) throw RuntimeError{name + ": horizon too large"};
   if (c->nx > kMaxNX || c->nu > kMaxNU || c->ny > kMaxNY) throw RuntimeError{"ModelDims: dimension exceeds capacity"};
 }
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+uint32_t tail_table_size(uint32_t* j_lo_out, uint32_t* j_hi_out);
 
 void fill_args(smpc_ctx* c) {
   IterArgs& a = c->base;
@@ -297,6 +301,13 @@ void fill_args(smpc_ctx* c) {
   a.lambda = p.lambda;
   a.key0 = (uint32_t)p.seed;
   a.key1 = (uint32_t)(p.seed >> 32);
+  for (int r = 0; r < 10; ++r) {  // Philox round keys (rng.hpp:24-25)
+    a.rk.k0[r] = a.key0 + (uint32_t)r * 0x9E3779B9u;
+    a.rk.k1[r] = a.key1 + (uint32_t)r * 0xBB67AE85u;
+  }
+  a.pk.one = 0x3f8000003f800000ull;    // {1.0f, 1.0f}
+  a.pk.mzero = 0x8000000080000000ull;  // {-0.0f, -0.0f}
+  tail_table_size(&a.j_lo, &a.j_hi);
   a.with_mean = p.include_mean_sample != 0;
   // zero-mean quota filled from the tail (sampling.cpp:56-62)
   long long n_zero = (long long)ceil(p.zero_mean_fraction * (double)c->M);
@@ -337,6 +348,7 @@ void fill_args(smpc_ctx* c) {
   a.outs_nom = reinterpret_cast<float*>(c->d_result + c->off_outs);
   a.do_finish = 0;
   a.normalize_weights = 0;
+  a.skip_w = p.update_skip_mass > 0.0 ? p.update_skip_mass / (double)c->M : 0.0;
   for (int i = 0; i < 8; ++i) a.dyn.p[i] = 0.f;
   switch (p.dynamics_kind) {
     case SMPC_DYN_CARTPOLE:
@@ -382,8 +394,15 @@ void fill_args(smpc_ctx* c) {
   }
 }
 
-// Number of entries of the Phi^-1 tail table (see philox_normal.cuh).
-uint32_t tail_table_size() {
+// Number of entries of the Phi^-1 tail table (see philox_normal.cuh), and the
+// integer thresholds: j is a lower tail iff j < *j_lo_out, upper iff j >= *j_hi_out.
+uint32_t tail_table_size(uint32_t* j_lo_out, uint32_t* j_hi_out) {
+  static uint32_t cached_lo = 0, cached_hi = 0, cached_n = 0;
+  if (cached_n) {
+    if (j_lo_out) *j_lo_out = cached_lo;
+    if (j_hi_out) *j_hi_out = cached_hi;
+    return cached_n;
+  }
   const float kLow = 0.02425f;
   const volatile float one = 1.0f;
   const float kHigh = one - kLow;
@@ -393,7 +412,12 @@ uint32_t tail_table_size() {
     if (pj < kLow) j_lo = j + 1;
     if (pj > kHigh && j < j_hi) j_hi = j;
   }
-  return std::max(j_lo, (1u << 23) - j_hi);
+  cached_lo = j_lo;
+  cached_hi = j_hi;
+  cached_n = std::max(j_lo, (1u << 23) - j_hi);
+  if (j_lo_out) *j_lo_out = j_lo;
+  if (j_hi_out) *j_hi_out = j_hi;
+  return cached_n;
 }
 
 void decode_error(smpc_ctx* c, unsigned long long key) {
@@ -634,7 +658,7 @@ smpc_status smpc_create(const smpc_problem* problem, smpc_ctx** out) {
       c->d_costmap = dalloc<uint8_t>(cells);
       if (!c->costmap.empty()) CK(cudaMemcpy(c->d_costmap, c->costmap.data(), cells, cudaMemcpyHostToDevice));
     }
-    const uint32_t n_tab = tail_table_size();
+    const uint32_t n_tab = tail_table_size(nullptr, nullptr);
     c->d_tail = dalloc<float>(n_tab);
     CK(build_tail_table(c->d_tail, n_tab, c->stream));
     c->host_mean[0].assign(TU, 0.f);

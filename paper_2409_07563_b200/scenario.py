@@ -80,6 +80,7 @@ class SmpcProblem(ctypes.Structure):
         ("device", ctypes.c_int32),
         ("shard_begin", ctypes.c_int64),
         ("shard_end", ctypes.c_int64),
+        ("update_skip_mass", ctypes.c_double),
     ]
 
 
@@ -195,6 +196,9 @@ class Scenario:
     nominal_reset_bound: float = math.inf
     initial_state: Dict[str, float] = dataclasses.field(default_factory=dict)
     device: int = 0
+    # B200 deployment knob (not in the reference schema): weighted-update
+    # samples with w_m < update_skip_mass / M are skipped (0 = exact).
+    update_skip_mass: float = 2.0 ** -64
 
     # --- derived -----------------------------------------------------------
     @property
@@ -306,6 +310,7 @@ class Scenario:
         p.device = int(self.device)
         if shard is not None:
             p.shard_begin, p.shard_end = int(shard[0]), int(shard[1])
+        p.update_skip_mass = float(self.update_skip_mass)
         p._keepalive = keep  # arrays must outlive the struct
         return p
 
