@@ -79,6 +79,7 @@ struct IterArgs {
   PhiloxKeys rk;         // round keys of (key0, key1)
   PackConst pk;
   uint32_t j_lo, j_hi;   // uniform index j = w >> 9 is a lower tail iff j < j_lo, upper iff j >= j_hi
+  uint32_t tail_hi_base; // N + 2^23 - 1: upper-tail entry of j is tail[tail_hi_base - j]
   int with_mean;
   long long zero_begin;
   int importance;

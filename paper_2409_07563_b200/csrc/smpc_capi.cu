@@ -307,7 +307,7 @@ void fill_args(smpc_ctx* c) {
   }
   a.pk.one = 0x3f8000003f800000ull;    // {1.0f, 1.0f}
   a.pk.mzero = 0x8000000080000000ull;  // {-0.0f, -0.0f}
-  tail_table_size(&a.j_lo, &a.j_hi);
+  a.tail_hi_base = tail_table_size(&a.j_lo, &a.j_hi) + (1u << 23) - 1u;
   a.with_mean = p.include_mean_sample != 0;
   // zero-mean quota filled from the tail (sampling.cpp:56-62)
   long long n_zero = (long long)ceil(p.zero_mean_fraction * (double)c->M);
@@ -659,7 +659,7 @@ smpc_status smpc_create(const smpc_problem* problem, smpc_ctx** out) {
       if (!c->costmap.empty()) CK(cudaMemcpy(c->d_costmap, c->costmap.data(), cells, cudaMemcpyHostToDevice));
     }
     const uint32_t n_tab = tail_table_size(nullptr, nullptr);
-    c->d_tail = dalloc<float>(n_tab);
+    c->d_tail = dalloc<float>(2 * (size_t)n_tab);
     CK(build_tail_table(c->d_tail, n_tab, c->stream));
     c->host_mean[0].assign(TU, 0.f);
     c->host_mean[1].assign(TU, 0.f);
