@@ -112,6 +112,9 @@ struct IterArgs {
   double* blk_eta;       // [S][n_w_blocks]
   long long* blk_nz;     // [S][n_w_blocks]
   double* gather2;       // [world][S][2]  (eta_g, nonzero_g)
+  int* cand;             // [S][M_local] update candidates, compacted per weights-CTA range
+  int* cand_cnt;         // [S][n_w_blocks]
+  long long* cand_off;   // [S][n_w_blocks + 1] exclusive prefix of cand_cnt
   int n_u_blocks;
   double* blk_part;      // [S][n_u_blocks][T*NU]
   double* gather3;       // [world][S][T*NU]

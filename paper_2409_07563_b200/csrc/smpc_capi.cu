@@ -109,6 +109,8 @@ struct smpc_ctx {
   double *d_sig2 = nullptr, *d_gamma = nullptr, *d_costs = nullptr, *d_weights = nullptr;
   double *d_blk_min = nullptr, *d_blk_eta = nullptr, *d_blk_part = nullptr;
   double *d_gather1 = nullptr, *d_gather2 = nullptr, *d_gather3 = nullptr;
+  int *d_cand = nullptr, *d_cand_cnt = nullptr;
+  long long* d_cand_off = nullptr;
   long long *d_blk_arg = nullptr, *d_blk_nz = nullptr;
   unsigned int* d_counters = nullptr;
   uint8_t* d_costmap = nullptr;
@@ -339,6 +341,9 @@ void fill_args(smpc_ctx* c) {
   a.blk_eta = c->d_blk_eta;
   a.blk_nz = c->d_blk_nz;
   a.gather2 = c->d_gather2;
+  a.cand = c->d_cand;
+  a.cand_cnt = c->d_cand_cnt;
+  a.cand_off = c->d_cand_off;
   a.n_u_blocks = c->n_u_blocks;
   a.blk_part = c->d_blk_part;
   a.gather3 = c->d_gather3;
@@ -604,7 +609,7 @@ smpc_status smpc_create(const smpc_problem* problem, smpc_ctx** out) {
 
     c->d_mean = dalloc<float>((size_t)c->S * TU);
     c->d_x0 = dalloc<float>((size_t)2 * kMaxNX);
-    c->d_sigma = dalloc<float>(TU);
+    c->d_sigma = dalloc<float>((size_t)(TU + 3) / 4 * 4);  // float4-readable
     c->d_sig2 = dalloc<double>(TU);
     c->d_gamma = dalloc<double>(c->T);
     c->d_costs = dalloc<double>((size_t)c->S * c->M_local);
@@ -613,6 +618,9 @@ smpc_status smpc_create(const smpc_problem* problem, smpc_ctx** out) {
     c->d_blk_arg = dalloc<long long>((size_t)c->S * c->n_roll_blocks);
     c->d_blk_eta = dalloc<double>((size_t)c->S * c->n_w_blocks);
     c->d_blk_nz = dalloc<long long>((size_t)c->S * c->n_w_blocks);
+    c->d_cand = dalloc<int>((size_t)c->S * c->M_local);
+    c->d_cand_cnt = dalloc<int>((size_t)c->S * c->n_w_blocks);
+    c->d_cand_off = dalloc<long long>((size_t)c->S * (c->n_w_blocks + 1));
     c->d_blk_part = dalloc<double>((size_t)c->S * c->n_u_blocks * TU);
     c->d_counters = dalloc<unsigned int>(16);
     c->d_gather1 = dalloc<double>((size_t)c->S * 2 * 8);
@@ -689,7 +697,8 @@ void smpc_destroy(smpc_ctx* c) {
   void* ptrs[] = {c->d_mean, c->d_x0, c->d_sigma, c->d_tail, c->d_sig2, c->d_gamma, c->d_costs,
                   c->d_weights, c->d_blk_min, c->d_blk_eta, c->d_blk_part, c->d_gather1, c->d_gather2,
                   c->d_gather3, c->d_blk_arg, c->d_blk_nz, c->d_counters, c->d_costmap, c->d_result,
-                  c->d_ro_x0, c->d_ro_mean, c->d_eps, c->d_outputs, c->d_wscratch, c->d_flags};
+                  c->d_ro_x0, c->d_ro_mean, c->d_eps, c->d_outputs, c->d_wscratch, c->d_flags,
+                  c->d_cand, c->d_cand_cnt, c->d_cand_off};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->h_result) cudaFreeHost(c->h_result);
@@ -962,7 +971,7 @@ smpc_status smpc_compute_weights(smpc_ctx* c, const double* costs, int64_t count
     for (int64_t m = 0; m < count; ++m)
       if (!std::isfinite(costs[m])) throw RuntimeError{"compute_weights: non-finite cost at sample " + std::to_string(m)};
     const int nblk = (int)std::min<long long>((count + 255) / 256, 148 * 4);
-    const size_t need = (size_t)2 * count + 4 * (size_t)nblk + 8;
+    const size_t need = (size_t)2 * count + 4 * (size_t)nblk + 8 + (size_t)count / 2 + 1 + 2 * (size_t)nblk + 2;
     if (c->wscratch_cap < need) {
       if (c->d_wscratch) cudaFree(c->d_wscratch);
       c->d_wscratch = dalloc<double>(need);
@@ -976,6 +985,9 @@ smpc_status smpc_compute_weights(smpc_ctx* c, const double* costs, int64_t count
     double* d_nz = d_eta + nblk;
     double* d_g1 = d_nz + nblk;  // [2]
     double* d_g2 = d_g1 + 2;     // [2]
+    int* d_cand = reinterpret_cast<int*>(d_g2 + 2);                         // [count]
+    int* d_ccnt = d_cand + count + (count & 1);                            // [nblk]
+    long long* d_coff = reinterpret_cast<long long*>(d_ccnt + nblk + (nblk & 1));  // [nblk+1]
     CK(cudaMemcpyAsync(d_costs, costs, sizeof(double) * count, cudaMemcpyHostToDevice, c->stream));
     CK(launch_begin_solve(c->header(), c->stream));
     CK(launch_min_only(d_costs, count, d_bmin, d_barg, nblk, c->d_counters + 8, d_g1,
@@ -993,6 +1005,9 @@ smpc_status smpc_compute_weights(smpc_ctx* c, const double* costs, int64_t count
     a.n_w_blocks = nblk;
     a.blk_eta = d_eta;
     a.blk_nz = reinterpret_cast<long long*>(d_nz);
+    a.cand = d_cand;
+    a.cand_cnt = d_ccnt;
+    a.cand_off = d_coff;
     CK(launch_weights(a, c->stream));
     CK(launch_normalize_weights(a, c->stream));
     double g1[2], g2[2];
