@@ -21,7 +21,7 @@ import numpy as np
 
 from . import _lib
 from ._lib import SmpcConfigError, SmpcError, check
-from .scenario import Scenario, SmpcSolution, SmpcTubeSolution, SmpcWeightSummary
+from .scenario import Scenario, SmpcSolution, SmpcTubeSolution, SmpcWeightSummary, shard_range
 
 __all__ = ["make_controller", "MppiController", "TubeMppiController", "RolloutEngine", "GaussianSampler",
            "ControllerSolution", "TubeSolution", "WeightResult", "SmpcError", "SmpcConfigError"]
@@ -246,3 +246,33 @@ def make_controller(scenario: Scenario, shard: Optional[tuple] = None) -> MppiCo
 
 def host_libm_uses_fma() -> bool:
     return bool(_lib.load().smpc_host_libm_uses_fma())
+
+
+class ShardGroup:
+    """n sample shards of one problem in this process (smpc_group_*): the
+    multi-GPU iteration (rank-indexed gathers, fixed-rank-order combine) with
+    device-to-device copies standing in for NCCL. devices: one ordinal per
+    shard (default: all on the scenario's device)."""
+
+    def __init__(self, scenario: Scenario, n: int, devices=None):
+        self.n = n
+        self.members = []
+        for r in range(n):
+            sc = dataclasses.replace(scenario)
+            if devices is not None:
+                sc.device = devices[r]
+            self.members.append(MppiController(sc, shard_range(scenario.num_samples, r, n)))
+        self.lib = self.members[0].lib
+        self._arr = (ctypes.c_void_p * n)(*[m.ctx.value for m in self.members])
+        check(self.lib.smpc_group_init(self._arr, n), self.members[0].ctx)
+
+    def compute_control(self, x0):
+        m0 = self.members[0]
+        sols, bufs = [], []
+        for m in self.members:
+            s, b = m._solution_struct(False)
+            sols.append(s)
+            bufs.append(b)
+        arr = (SmpcSolution * self.n)(*sols)
+        check(self.lib.smpc_group_compute_control(self._arr, self.n, _f32(x0).ravel(), arr), m0.ctx)
+        return [m._wrap(arr[i], bufs[i]) for i, m in enumerate(self.members)]

@@ -129,6 +129,7 @@ struct smpc_ctx {
   int n_roll_blocks = 1, n_w_blocks = 1, n_u_blocks = 1;
   // graph
   cudaGraphExec_t graph = nullptr;
+  cudaEvent_t ev_stage = nullptr;
   bool timing = false;
   std::vector<cudaEvent_t> ev;
   double rollout_ms_total = 0.0;
@@ -481,6 +482,57 @@ void enqueue_solve(smpc_ctx* c, bool timed) {
   CK(launch_finish_solve(c->header(), c->stream));
 }
 
+// ---- in-process shard group (one host thread, any devices) ------------------
+// The same kernels and the same rank-indexed gather buffers as the NCCL path;
+// each all-gather is done as device-to-device copies of every rank's slot into
+// every rank's buffer, ordered with events. Used to run (and test) the
+// world > 1 combine logic on a single GPU.
+void group_allgather(smpc_ctx** cs, int n, int which) {
+  for (int r = 0; r < n; ++r) CK(cudaEventRecord(cs[r]->ev_stage, cs[r]->stream));
+  for (int d = 0; d < n; ++d) {
+    smpc_ctx* dst = cs[d];
+    for (int r = 0; r < n; ++r) {
+      smpc_ctx* src = cs[r];
+      if (r == d) continue;
+      CK(cudaStreamWaitEvent(dst->stream, src->ev_stage, 0));
+      size_t slot;
+      double *from, *to;
+      if (which == 1) {
+        slot = (size_t)src->S * 2;
+        from = src->d_gather1, to = dst->d_gather1;
+      } else if (which == 2) {
+        slot = (size_t)src->S * 2;
+        from = src->d_gather2, to = dst->d_gather2;
+      } else {
+        slot = (size_t)src->S * src->T * src->nu;
+        from = src->d_gather3, to = dst->d_gather3;
+      }
+      CK(cudaMemcpyAsync(to + r * slot, from + r * slot, slot * sizeof(double), cudaMemcpyDefault, dst->stream));
+    }
+  }
+}
+
+void enqueue_group_solve(smpc_ctx** cs, int n) {
+  for (int r = 0; r < n; ++r) CK(launch_begin_solve(cs[r]->header(), cs[r]->stream));
+  const int I = cs[0]->I;
+  for (int it = 0; it < I; ++it) {
+    auto args = [&](smpc_ctx* c) {
+      IterArgs a = c->base;
+      a.iter = it;
+      a.do_finish = it == I - 1;
+      return a;
+    };
+    for (int r = 0; r < n; ++r) CK(cs[r]->ops.rollout(args(cs[r]), cs[r]->p.cost_kind, cs[r]->stream));
+    group_allgather(cs, n, 1);
+    for (int r = 0; r < n; ++r) CK(cs[r]->ops.weights(args(cs[r]), cs[r]->stream));
+    group_allgather(cs, n, 2);
+    for (int r = 0; r < n; ++r) CK(cs[r]->ops.update(args(cs[r]), cs[r]->stream));
+    group_allgather(cs, n, 3);
+    for (int r = 0; r < n; ++r) CK(cs[r]->ops.combine(args(cs[r]), cs[r]->stream));
+  }
+  for (int r = 0; r < n; ++r) CK(launch_finish_solve(cs[r]->header(), cs[r]->stream));
+}
+
 void build_graph(smpc_ctx* c) {
   if (c->graph) {
     cudaGraphExecDestroy(c->graph);
@@ -672,6 +724,7 @@ smpc_status smpc_create(const smpc_problem* problem, smpc_ctx** out) {
     c->host_mean[0].assign(TU, 0.f);
     c->host_mean[1].assign(TU, 0.f);
     c->nominal_state.assign(c->nx, 0.f);
+    CK(cudaEventCreateWithFlags(&c->ev_stage, cudaEventDisableTiming));
     for (int i = 0; i < 2 * c->I; ++i) {
       cudaEvent_t e;
       CK(cudaEventCreate(&e));
@@ -693,6 +746,7 @@ void smpc_destroy(smpc_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->graph) cudaGraphExecDestroy(c->graph);
   for (auto e : c->ev) cudaEventDestroy(e);
+  if (c->ev_stage) cudaEventDestroy(c->ev_stage);
   if (c->comm && nccl()) nccl()->CommDestroy(c->comm);
   void* ptrs[] = {c->d_mean, c->d_x0, c->d_sigma, c->d_tail, c->d_sig2, c->d_gamma, c->d_costs,
                   c->d_weights, c->d_blk_min, c->d_blk_eta, c->d_blk_part, c->d_gather1, c->d_gather2,
@@ -1071,6 +1125,45 @@ smpc_status smpc_rollout_kernel_ms(smpc_ctx* c, int32_t enable, double* total_ms
     c->rollout_launches = 0;
   }
   return SMPC_OK;
+}
+
+smpc_status smpc_group_init(smpc_ctx** ctxs, int32_t n) {
+  if (!ctxs || n < 1 || n > 8) return SMPC_ERR_ARGUMENT;
+  for (int r = 0; r < n; ++r)
+    if (!ctxs[r]) return SMPC_ERR_ARGUMENT;
+  return guarded(ctxs[0], [&] {
+    for (int r = 0; r < n; ++r) {
+      smpc_ctx* c = ctxs[r];
+      if (c->M != ctxs[0]->M || c->T != ctxs[0]->T || c->S != ctxs[0]->S || c->I != ctxs[0]->I)
+        throw ConfigError{"smpc_group_init: contexts describe different problems"};
+      c->rank = r;
+      c->world = n;
+      fill_args(c);
+      if (c->graph) {
+        cudaGraphExecDestroy(c->graph);
+        c->graph = nullptr;
+      }
+    }
+  });
+}
+
+smpc_status smpc_group_compute_control(smpc_ctx** ctxs, int32_t n, const float* x0, smpc_solution* out) {
+  if (!ctxs || n < 1 || !x0) return SMPC_ERR_ARGUMENT;
+  return guarded(ctxs[0], [&] {
+    const double t0 = now_ms();
+    for (int r = 0; r < n; ++r) {
+      if (ctxs[r]->world != n || ctxs[r]->rank != r) throw ConfigError{"smpc_group_compute_control: call smpc_group_init first"};
+      upload_x0(ctxs[r], x0, ctxs[r]->S);
+    }
+    enqueue_group_solve(ctxs, n);
+    for (int r = 0; r < n; ++r) fetch_results(ctxs[r]);
+    for (int r = 0; r < n; ++r) {
+      if (out) {
+        copy_solution(ctxs[r], 0, &out[r]);
+        out[r].solve_time_ms = now_ms() - t0;
+      }
+    }
+  });
 }
 
 smpc_status smpc_comm_unique_id(uint8_t id_out[128]) {

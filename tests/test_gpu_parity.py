@@ -246,3 +246,27 @@ def test_full_size_di_swarm_properties(mods):
         e, _ = O.generate_samples(sub, np.zeros((100, 2), np.float32), 0, m_begin=int(m), m_end=int(m) + 1)
         acc += w[m] * e[0].astype(np.float64)
     assert close(sol.controls, acc.astype(np.float32))
+
+
+@pytest.mark.parametrize("n", [2, 3, 8])
+@pytest.mark.parametrize("name", ["cartpole", "double_integrator", "unicycle_road"])
+def test_shard_group_matches_single(mods, name, n):
+    """World > 1 device path (gathers + rank-ordered combine) on one GPU:
+    rho/argmin exact, U* within tolerance, every rank bitwise identical."""
+    sc = scenarios(mods["S"])[name]
+    grp = mods["C"].ShardGroup(sc, n)
+    ref = mods["OracleController"](sc, "port")
+    x0 = sc.x0()
+    for solve in range(2):
+        sols = grp.compute_control(x0)
+        b = ref.compute_control(x0)
+        for s in sols[1:]:
+            assert np.array_equal(s.controls, sols[0].controls)
+            assert np.array_equal(s.states, sols[0].states)
+        a = sols[0]
+        assert a.weights.baseline == b["baseline"] and a.weights.argmin == b["argmin"]
+        assert close(a.weights.normalizer, b["normalizer"])
+        assert close(a.controls, b["controls"])
+        assert close(a.states, b["states"])
+        for m in grp.members:
+            m.set_mean(b["controls"])
