@@ -148,6 +148,7 @@ ModelOps ops_double_integrator();
 
 cudaError_t build_tail_table(float* table, uint32_t n, cudaStream_t stream);
 cudaError_t launch_begin_solve(ResultHeader* h, cudaStream_t stream);
+cudaError_t launch_icdf_domain(const IterArgs& a, float* out, cudaStream_t stream);
 cudaError_t launch_finish_solve(ResultHeader* h, cudaStream_t stream);
 cudaError_t launch_weights(const IterArgs& a, cudaStream_t stream);
 cudaError_t launch_normalize_weights(const IterArgs& a, cudaStream_t stream);

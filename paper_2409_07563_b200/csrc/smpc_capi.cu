@@ -1115,6 +1115,17 @@ int32_t smpc_kernels_per_solve(const smpc_ctx* c) {
   return 2 + c->I * (3 + (c->world > 1 ? 1 : 0));
 }
 
+smpc_status smpc_icdf_domain(smpc_ctx* c, float* out) {
+  if (!c || !out) return SMPC_ERR_ARGUMENT;
+  return guarded(c, [&] {
+    float* d = dalloc<float>(1u << 23);
+    CK(launch_icdf_domain(c->base, d, c->stream));
+    CK(cudaMemcpyAsync(out, d, sizeof(float) << 23, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    cudaFree(d);
+  });
+}
+
 smpc_status smpc_rollout_kernel_ms(smpc_ctx* c, int32_t enable, double* total_ms, int64_t* launches) {
   if (!c) return SMPC_ERR_ARGUMENT;
   if (total_ms) *total_ms = c->rollout_ms_total;

@@ -68,6 +68,18 @@ def test_tail_table_and_icdf_exhaustive(mods):
     assert np.isin(eps_d.ravel(), ref).all()
 
 
+def test_icdf_whole_domain_bit_exact(mods):
+    """normal_icdf(to_open_unit(w)) on the device — packed Acklam central
+    branch, packed Markstein division, tail table — equals the reference for
+    ALL 2^23 possible uniforms."""
+    ref = mods["Oracle"]("port").icdf_domain()
+    eng = mods["C"].RolloutEngine(mods["S"].cartpole_scenario(num_samples=16, horizon=4))
+    out = np.zeros(1 << 23, np.float32)
+    eng._check(eng.lib.smpc_icdf_domain(eng.ctx, out))
+    bad = np.nonzero(out.view(np.uint32) != ref.view(np.uint32))[0]
+    assert bad.size == 0, (bad[:10], out[bad[:10]], ref[bad[:10]])
+
+
 @pytest.mark.parametrize("name", ["cartpole", "double_integrator", "diff_drive_nav", "unicycle_road",
                                   "cartpole_road_perstep", "di_quadratic_dmd"])
 def test_generate_samples_bit_exact(mods, name):
