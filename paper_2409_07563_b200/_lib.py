@@ -43,10 +43,12 @@ class SmpcConfigError(SmpcError):
     """smpc::ConfigError."""
 
 
-def load(path: str = LIB_PATH) -> ctypes.CDLL:
+def load(path: str = None) -> ctypes.CDLL:
+    """Load the library (SMPC_B200_LIB overrides the in-tree path, for A/B runs)."""
     global _lib
     if _lib is not None:
         return _lib
+    path = path or os.environ.get("SMPC_B200_LIB", LIB_PATH)
     if not os.path.exists(path):
         raise ImportError(f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
                           " (there is no CPU fallback)")

@@ -8,19 +8,37 @@
 
 namespace smpc_dev {
 
-inline RoadCostDev make_road(const CostParams& c) { return RoadCostDev{c.p[0], c.p[1], c.p[2]}; }
+inline RoadCostDev make_road(const CostParams& c) {
+  RoadCostDev r;
+  r.half_width = c.p[0];
+  r.lin_d = (double)c.p[1];
+  r.quad_d = (double)c.p[2];
+  r.lin_hw_d = r.lin_d * (double)c.p[0];  // static_cast<double>(linear) * half_width (costs.cpp:40)
+  return r;
+}
 
 // CircleTrackCost ctor precomputes the squared radii in float (costs.cpp:50-51).
 inline CircleTrackCostDev make_circle(const CostParams& c) {
   volatile float inner = c.p[0], outer = c.p[1];
-  const float inner_sq = inner * inner, outer_sq = outer * outer;
-  return CircleTrackCostDev{inner_sq, outer_sq, c.p[2], c.p[3], c.p[4], c.p[5], c.p[6]};
+  CircleTrackCostDev k;
+  k.inner_sq = inner * inner;
+  k.outer_sq = outer * outer;
+  k.speed_target = c.p[3];
+  k.am_target = c.p[5];
+  volatile double zero = 0.0;
+  k.crash0_d = zero + (double)c.p[2];  // cost = 0.0; cost += crash (costs.cpp:57-58)
+  k.speed_coeff_d = (double)c.p[4];
+  k.am_coeff_d = (double)c.p[6];
+  return k;
 }
 
 inline NavCostDev make_nav(const CostParams& c) {
   NavCostDev n;
   n.goal_x = c.p[0], n.goal_y = c.p[1], n.goal_yaw = c.p[2];
-  n.dist_coeff = c.p[3], n.yaw_coeff = c.p[4], n.obstacle_cost = c.p[5];
+  n.dist_d = (double)c.p[3], n.yaw_d = (double)c.p[4];
+  volatile double one = 1.0, zero = 0.0;  // occupancy() returns 1.0f / 0.0f
+  n.obst_occ_d = (double)c.p[5] * one;
+  n.obst_free_d = (double)c.p[5] * zero;
   n.origin_x = c.origin_x, n.origin_y = c.origin_y, n.inv_resolution = c.inv_resolution;
   n.cells_x = c.cells_x, n.cells_y = c.cells_y;
   n.grid = c.grid;
@@ -30,7 +48,7 @@ inline NavCostDev make_nav(const CostParams& c) {
 template <int NY>
 inline QuadraticCostDev<NY> make_quad(const CostParams& c) {
   QuadraticCostDev<NY> q;
-  for (int i = 0; i < NY; ++i) q.target[i] = c.target[i], q.weights[i] = c.weights[i];
+  for (int i = 0; i < NY; ++i) q.target_d[i] = (double)c.target[i], q.weights_d[i] = (double)c.weights[i];
   return q;
 }
 
