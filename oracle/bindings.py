@@ -79,6 +79,8 @@ class Oracle:
             L.oracle_compute_control.argtypes = [ctypes.POINTER(SmpcProblem), _f32p, ctypes.POINTER(ctypes.c_uint64),
                                                  _f32p, _f32p, _f32p, _f32p, ctypes.c_void_p,
                                                  ctypes.POINTER(SmpcWeightSummary), ctypes.POINTER(_OracleErr)]
+            L.oracle_partial_sort.argtypes = [_f64p, ctypes.c_int64, ctypes.c_int64,
+                                              np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS")]
             L.oracle_running_cost.argtypes = [ctypes.POINTER(SmpcProblem), _f32p]
             L.oracle_running_cost.restype = ctypes.c_double
             L.oracle_terminal_cost.argtypes = [ctypes.POINTER(SmpcProblem), _f32p]
@@ -225,6 +227,13 @@ class Oracle:
         self._check(rc, buf.value)
         return w, rho.value, eta.value, int(np.argmin(costs))
 
+    def partial_sort(self, costs, k: int) -> np.ndarray:
+        """First k of std::partial_sort with CemController's comparator (controllers.cpp:165-171)."""
+        costs = np.ascontiguousarray(costs, np.float64)
+        out = np.zeros(k, np.int64)
+        self.lib.oracle_partial_sort(costs, costs.size, k, out)
+        return out
+
     def weighted_update(self, mean, eps, weights, step_sizes=()):
         T, n_u = mean.shape
         out = np.zeros(T * n_u, np.float32)
@@ -301,7 +310,9 @@ class OracleController:
             rc = self.o.lib.ref_compute_control(self.handle, x0, controls, states, outputs, w.ctypes.data, s4, buf, 512)
             Oracle._check(rc, buf.value)
             self.o.lib.ref_get_mean(self.handle, self.mean)
-            summary = dict(baseline=s4[0], normalizer=s4[1], argmin=int(s4[2]), nonzero=int(np.count_nonzero(w)),
+            # the shim derives argmin from the first maximum weight: not the argmin for CEM's flat 1/k weights
+            argmin = -1 if sc.controller == "cem" else int(s4[2])
+            summary = dict(baseline=s4[0], normalizer=s4[1], argmin=argmin, nonzero=int(np.count_nonzero(w)),
                            solve_time_ms=s4[3])
         return dict(controls=controls.reshape(T, n_u), states=states.reshape(T + 1, n_x),
                     outputs=outputs.reshape(T, n_y), weights=weights, **summary)

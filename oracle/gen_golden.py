@@ -46,6 +46,15 @@ def fixture_scenarios():
     circle = S.di_swarm_scenario(num_samples=256, horizon=32, seed=7)
     circle.controller, circle.step_size = "dmd", 0.8  # proj/configs/circle_track_dmd.json
     sc["circle_track_dmd_config"] = circle
+    # CemController (controllers.cpp:149-203); importance on in the config to
+    # pin that CEM ranks the raw costs
+    sc["di_quadratic_cem"] = S.Scenario(num_samples=192, horizon=25, dynamics="double_integrator", cost="quadratic",
+                                        target=[1.0, -1.0, 0.0, 0.0], weights=[1.0, 1.0, 0.1, 0.1], rng_seed=9,
+                                        control_std=(0.7, 0.4), controller="cem", elite_fraction=0.25,
+                                        zero_mean_fraction=0.1)
+    cem_c1 = S.cartpole_scenario(num_samples=300, horizon=60, seed=2)
+    cem_c1.controller, cem_c1.elite_fraction = "cem", 0.07
+    sc["cartpole_cem"] = cem_c1
     tube = S.cartpole_scenario(num_samples=256, horizon=50, seed=4)
     tube.controller = "tube"
     sc["cartpole_tube"] = tube

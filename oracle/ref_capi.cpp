@@ -320,6 +320,10 @@ void* ref_controller_create(const smpc_problem* p, int workers, int strategy, ch
                                                      p->nominal_reset_bound,
                                                      engine_cfg(workers, strategy));
       rc->tube = true;
+    } else if (p->controller_kind == SMPC_CTRL_CEM) {
+      CemSettings cem;
+      cem.elite_fraction = p->elite_fraction;
+      rc->ctl = std::make_unique<CemController>(dyn, cost, sc, settings(p), cem, engine_cfg(workers, strategy));
     } else {
       rc->ctl = std::make_unique<MppiController>(dyn, cost, sc, settings(p),
                                                  engine_cfg(workers, strategy),

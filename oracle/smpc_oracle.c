@@ -547,7 +547,66 @@ static int iterate(const smpc_problem* p, const oracle_dims* d, int S, const flo
   return rc;
 }
 
-/* MppiController::compute_control (controllers.cpp:113-135). */
+/* The CEM comparator (controllers.cpp:165-171): cost, then lower index. */
+static const double* g_sort_costs; /* qsort has no context argument; test-only, single-threaded */
+static int cem_cmp(const void* pa, const void* pb) {
+  const int64_t a = *(const int64_t*)pa, b = *(const int64_t*)pb;
+  const double ca = g_sort_costs[a], cb = g_sort_costs[b];
+  if (ca != cb) return ca < cb ? -1 : 1;
+  return a < b ? -1 : (a > b);
+}
+
+/* std::partial_sort(order, order + k, order + n, cmp) (controllers.cpp:165-171):
+ * the comparator is a strict total order, so the first k of a full sort are
+ * exactly partial_sort's first k. */
+void oracle_partial_sort(const double* costs, int64_t n, int64_t k, int64_t* order_out) {
+  int64_t* order = (int64_t*)malloc(sizeof(int64_t) * (size_t)n);
+  for (int64_t i = 0; i < n; ++i) order[i] = i;
+  g_sort_costs = costs;
+  qsort(order, (size_t)n, sizeof(int64_t), cem_cmp);
+  memcpy(order_out, order, sizeof(int64_t) * (size_t)k);
+  free(order);
+}
+
+/* One CemController iteration (controllers.cpp:153-199): rollout without the
+ * importance adjustment, elite average of the noise in sorted-elite order. */
+static int iterate_cem(const smpc_problem* p, const oracle_dims* d, const float* x0, float* mean,
+                       uint32_t stream, double* weights, smpc_weight_summary* sm, oracle_error* err) {
+  const int M = p->num_samples, T = p->horizon, n_u = d->n_u;
+  const size_t K = (size_t)T * n_u;
+  float* eps = (float*)malloc(sizeof(float) * (size_t)M * K);
+  double* costs = (double*)malloc(sizeof(double) * (size_t)M);
+  int rc = oracle_generate_samples(p, mean, 0, M, stream, eps, NULL, err);
+  if (!rc) rc = oracle_rollout(p, 1, x0, mean, eps, 0, M, NULL, costs, NULL, err);
+  if (!rc) {
+    int k = (int)ceil(p->elite_fraction * M); /* std::max(1, (int)std::ceil(f * M)) (:164) */
+    if (k < 1) k = 1;
+    int64_t* order = (int64_t*)malloc(sizeof(int64_t) * (size_t)k);
+    oracle_partial_sort(costs, M, k, order);
+    double* acc = (double*)calloc(K, sizeof(double));
+    for (int i = 0; i < k; ++i) {
+      const float* row = &eps[(size_t)order[i] * K];
+      for (size_t j = 0; j < K; ++j) acc[j] += row[j];
+    }
+    for (size_t j = 0; j < K; ++j) mean[j] = (float)(mean[j] + acc[j] / k);
+    sm->baseline = costs[order[0]];
+    sm->normalizer = (double)k;
+    sm->argmin = order[0];
+    sm->nonzero = k;
+    if (weights) {
+      for (int m = 0; m < M; ++m) weights[m] = 0.0;
+      for (int i = 0; i < k; ++i) weights[order[i]] = 1.0 / k;
+    }
+    free(acc);
+    free(order);
+  }
+  free(eps);
+  free(costs);
+  return rc;
+}
+
+/* MppiController::compute_control (controllers.cpp:113-135); CemController
+ * (controllers.cpp:149-203) when p->controller_kind == SMPC_CTRL_CEM. */
 int oracle_compute_control(const smpc_problem* p, float* mean, uint64_t* solve_count,
                            const float* x0, float* controls, float* states, float* outputs,
                            double* weights, smpc_weight_summary* summary, oracle_error* err) {
@@ -557,7 +616,9 @@ int oracle_compute_control(const smpc_problem* p, float* mean, uint64_t* solve_c
   smpc_weight_summary sm = {0};
   for (int iter = 0; iter < p->iterations; ++iter) {
     const uint32_t stream = (uint32_t)(*solve_count * 256u + (uint64_t)iter); /* :63-66 */
-    const int rc = iterate(p, &d, 1, x0, mean, stream, weights, &sm, err);
+    const int rc = p->controller_kind == SMPC_CTRL_CEM
+                       ? iterate_cem(p, &d, x0, mean, stream, weights, &sm, err)
+                       : iterate(p, &d, 1, x0, mean, stream, weights, &sm, err);
     if (rc) return rc;
   }
   ++*solve_count;

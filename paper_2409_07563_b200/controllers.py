@@ -136,7 +136,8 @@ class GaussianSampler(_Context):
 
 
 class MppiController(RolloutEngine):
-    """MppiController (also DMD: step sizes via the scenario)."""
+    """MppiController (also DMD: step sizes via the scenario; CemController:
+    elite selection via controller="cem", controllers.cpp:149-203)."""
 
     def set_mean(self, mean, system: int = 0) -> None:
         self._check(self.lib.smpc_set_mean(self.ctx, system, _f32(mean).ravel()))
@@ -189,6 +190,15 @@ class MppiController(RolloutEngine):
         self._check(self.lib.smpc_compute_control(self.ctx, _f32(x0).ravel(), ctypes.byref(sol)))
         return self._wrap(sol, bufs)
 
+    def sorted_samples(self, count: int, system: int = 0):
+        """(order, costs) of the first `count` samples of the last rollout in
+        (cost, index) order — std::partial_sort with CemController's
+        comparator (controllers.cpp:165-171), on the device."""
+        order = np.zeros(count, np.int64)
+        costs = np.zeros(count, np.float64)
+        self._check(self.lib.smpc_sorted_samples(self.ctx, system, int(count), order.ctypes.data, costs.ctypes.data))
+        return order, costs
+
     # --- device-resident replay (bench) -----------------------------------
     def set_x0(self, x0) -> None:
         self._check(self.lib.smpc_set_x0(self.ctx, _f32(x0).ravel()))
@@ -236,10 +246,10 @@ class TubeMppiController(MppiController):
 
 
 def make_controller(scenario: Scenario, shard: Optional[tuple] = None) -> MppiController:
-    """make_controller (controllers.cpp:294-344): mppi | dmd | tube."""
+    """make_controller (controllers.cpp:294-344): mppi | dmd | cem | tube."""
     if scenario.controller == "tube":
         return TubeMppiController(scenario, shard)
-    if scenario.controller in ("mppi", "dmd"):
+    if scenario.controller in ("mppi", "dmd", "cem"):
         return MppiController(scenario, shard)
     raise SmpcConfigError(2, f"controller.kind '{scenario.controller}' is not recognized")
 

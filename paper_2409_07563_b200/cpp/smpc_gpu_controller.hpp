@@ -69,8 +69,11 @@ inline Problem make_problem(const ScenarioConfig& sc, int device = 0) {
   p.include_mean_sample = sc.sampler.include_mean_sample ? 1 : 0;
   p.importance_sampling = sc.sampler.importance_sampling ? 1 : 0;
   const std::string& ck = sc.controller.kind;
-  p.controller_kind = ck == "dmd" ? SMPC_CTRL_DMD : ck == "tube" ? SMPC_CTRL_TUBE : SMPC_CTRL_MPPI;
-  if (ck != "mppi" && ck != "dmd" && ck != "tube")
+  p.controller_kind = ck == "dmd"    ? SMPC_CTRL_DMD
+                      : ck == "tube" ? SMPC_CTRL_TUBE
+                      : ck == "cem"  ? SMPC_CTRL_CEM
+                                     : SMPC_CTRL_MPPI;
+  if (ck != "mppi" && ck != "dmd" && ck != "tube" && ck != "cem")
     throw ConfigError("controller.kind '" + ck + "' is not recognized");
   if (ck == "dmd") {  // controllers.cpp:315-321
     if (!sc.controller.step_size_per_step.empty()) {
@@ -80,6 +83,7 @@ inline Problem make_problem(const ScenarioConfig& sc, int device = 0) {
     }
   }
   p.nominal_reset_bound = sc.controller.nominal_reset_bound;
+  p.elite_fraction = sc.controller.elite_fraction;
   const DynamicsSection& d = sc.dynamics;
   if (d.kind == "unicycle") {
     p.dynamics_kind = SMPC_DYN_UNICYCLE;
@@ -150,8 +154,9 @@ inline Problem make_problem(const ScenarioConfig& sc, int device = 0) {
   return out;
 }
 
-/// MppiController / DMD on the B200: drop-in for smpc::MppiController
-/// (controllers.hpp:89-97).
+/// MppiController / DMD / CemController on the B200: drop-in for
+/// smpc::MppiController (controllers.hpp:89-97) and smpc::CemController
+/// (controllers.hpp:103-116).
 class GpuMppiController : public Controller {
  public:
   GpuMppiController(const ScenarioConfig& scenario, int device = 0, double update_skip_mass = 0.0)
@@ -333,7 +338,9 @@ inline std::shared_ptr<Controller> make_gpu_controller(const ScenarioConfig& sce
   }
   if (scenario.controller.kind == "tube")
     return std::make_shared<GpuTubeMppiController>(scenario, device, update_skip_mass);
-  if (scenario.controller.kind == "mppi" || scenario.controller.kind == "dmd")
+  // mppi / dmd / cem share the single-system context; CEM's elite selection
+  // replaces the softmin weights on the device (controllers.cpp:149-203).
+  if (scenario.controller.kind == "mppi" || scenario.controller.kind == "dmd" || scenario.controller.kind == "cem")
     return std::make_shared<GpuMppiController>(scenario, device, update_skip_mass);
   throw ConfigError("controller.kind '" + scenario.controller.kind + "' is not recognized");
 }

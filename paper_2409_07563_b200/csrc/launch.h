@@ -8,9 +8,9 @@
 
 namespace smpc_dev {
 
-constexpr int kMaxNX = 8;
+constexpr int kMaxNX = 16;
 constexpr int kMaxNU = 4;
-constexpr int kMaxNY = 8;
+constexpr int kMaxNY = 16;
 constexpr int kRolloutThreads = 128;
 constexpr int kUpdateThreads = 256;
 constexpr int kUpdateWarps = kUpdateThreads / 32;
@@ -43,6 +43,7 @@ struct PackConst {
 // Model / cost parameters as plain floats (device functors are built from these).
 struct DynParams {
   float p[8];
+  const float* tensor;  // device copy of smpc_problem::dyn_tensor (SMPC_DYN_MLP)
 };
 struct CostParams {
   float p[8];
@@ -53,6 +54,14 @@ struct CostParams {
   int cells_x, cells_y;
   float origin_x, origin_y, inv_resolution;
   int map_in_smem;
+};
+
+// Radix-select state (select.cu): the k-th smallest (cost, index) key.
+struct SelectState {
+  unsigned long long prefix;  // threshold key K* (complete after the 8 passes)
+  long long k_rem;            // elites with key == K* (lowest indices first)
+  long long k;                // elites in total
+  unsigned int hist[256];
 };
 
 // Per-context iteration state on the device.
@@ -126,6 +135,7 @@ struct IterArgs {
   int do_finish;    // final iteration of a solve: nominal rollout + solve_count++
   int normalize_weights;  // write w = e/eta back (only when the caller wants weights)
   double skip_w;          // update skips samples with w_m < skip_w (0 = exact)
+  double cem_k;           // CEM: elite count k (commit mean + acc / k); 0 = MPPI / Tube
   DynParams dyn;
   CostParams cost;
 };
@@ -146,6 +156,10 @@ ModelOps ops_cartpole(bool fma_libm);
 ModelOps ops_diff_drive(bool fma_libm);
 ModelOps ops_double_integrator();
 
+cudaError_t launch_select(const IterArgs& a, SelectState* st, long long k, unsigned int* counters, int* eq_cnt,
+                          long long* eq_off, cudaStream_t stream);
+cudaError_t launch_sort_selected(const IterArgs& a, long long k, unsigned long long* keys, long long* idx,
+                                 unsigned long long* slot, cudaStream_t stream);
 cudaError_t build_tail_table(float* table, uint32_t n, cudaStream_t stream);
 cudaError_t launch_begin_solve(ResultHeader* h, cudaStream_t stream);
 cudaError_t launch_icdf_domain(const IterArgs& a, float* out, cudaStream_t stream);

@@ -90,7 +90,7 @@ T* dalloc(size_t n) {
 }
 
 const char* controller_name(int kind) {
-  return kind == SMPC_CTRL_DMD ? "dmd" : kind == SMPC_CTRL_TUBE ? "tube" : "mppi";
+  return kind == SMPC_CTRL_DMD ? "dmd" : kind == SMPC_CTRL_TUBE ? "tube" : kind == SMPC_CTRL_CEM ? "cem" : "mppi";
 }
 
 }  // namespace
@@ -114,6 +114,12 @@ struct smpc_ctx {
   long long *d_blk_arg = nullptr, *d_blk_nz = nullptr;
   unsigned int* d_counters = nullptr;
   uint8_t* d_costmap = nullptr;
+  float* d_dyn_tensor = nullptr;
+  // CEM elite selection / sample ordering (select.cu)
+  SelectState* d_select = nullptr;
+  int* d_eq_cnt = nullptr;
+  long long* d_eq_off = nullptr;
+  long long cem_k = 0;
   unsigned char* d_result = nullptr;
   unsigned char* h_result = nullptr;  // pinned
   size_t result_bytes = 0, off_controls = 0, off_states = 0, off_outs = 0;
@@ -216,7 +222,7 @@ void validate(smpc_ctx* c) {
   }
   c->nx = c->ops.nx, c->nu = c->ops.nu, c->ny = c->ops.ny;
   if (p.controller_kind != SMPC_CTRL_MPPI && p.controller_kind != SMPC_CTRL_DMD &&
-      p.controller_kind != SMPC_CTRL_TUBE)
+      p.controller_kind != SMPC_CTRL_TUBE && p.controller_kind != SMPC_CTRL_CEM)
     throw ConfigError{"controller.kind is not recognized"};
   // cost (make_cost + ctor checks)
   int cost_ny = c->ny, cost_nu = c->nu;
@@ -282,6 +288,8 @@ void validate(smpc_ctx* c) {
       throw RuntimeError{name + ": step sizes must be in (0, 1]"};
   if (p.controller_kind == SMPC_CTRL_TUBE && !(p.nominal_reset_bound > 0.0))
     throw RuntimeError{"tube: nominal_reset_bound must be > 0"};
+  if (p.controller_kind == SMPC_CTRL_CEM && !(p.elite_fraction > 0.0 && p.elite_fraction <= 1.0))
+    throw RuntimeError{"cem: elite_fraction must be in (0, 1]"};  // controllers.cpp:145-147
   if (!(p.update_skip_mass >= 0.0 && p.update_skip_mass < 1e-6))
     throw RuntimeError{name + ": update_skip_mass must be in [0, 1e-6)"};
   if (p.horizon > (1 << 22)) throw RuntimeError{name + ": horizon too large"};
@@ -316,7 +324,9 @@ void fill_args(smpc_ctx* c) {
   long long n_zero = (long long)ceil(p.zero_mean_fraction * (double)c->M);
   n_zero = std::min(n_zero, a.with_mean ? c->M - 1 : c->M);
   a.zero_begin = c->M - n_zero;
-  a.importance = p.importance_sampling != 0;
+  // CEM ranks raw rollout costs: no importance adjustment (controllers.cpp:155-162).
+  a.importance = p.importance_sampling != 0 && p.controller_kind != SMPC_CTRL_CEM;
+  a.cem_k = p.controller_kind == SMPC_CTRL_CEM ? (double)c->cem_k : 0.0;
   a.world = c->world;
   a.rank = c->rank;
   a.solve_count = &c->header()->solve_count;
@@ -460,6 +470,11 @@ void enqueue_solve(smpc_ctx* c, bool timed) {
     if (timed) CK(cudaEventRecord(c->ev[2 * it], c->stream));
     CK(c->ops.rollout(a, c->p.cost_kind, c->stream));
     if (timed) CK(cudaEventRecord(c->ev[2 * it + 1], c->stream));
+    if (c->p.controller_kind == SMPC_CTRL_CEM) {  // elite selection replaces compute_weights
+      CK(launch_select(a, c->d_select, c->cem_k, c->d_counters + 8, c->d_eq_cnt, c->d_eq_off, c->stream));
+      CK(c->ops.update(a, c->stream));
+      continue;
+    }
     if (c->world > 1) {
       const size_t n1 = (size_t)c->S * 2;
       if (nccl()->AllGather(c->d_gather1 + c->rank * n1, c->d_gather1, n1, ncclFloat64, c->comm, c->stream))
@@ -635,6 +650,8 @@ smpc_status smpc_create(const smpc_problem* problem, smpc_ctx** out) {
     c->I = p.iterations;
     c->M = p.num_samples;
     c->S = p.controller_kind == SMPC_CTRL_TUBE ? 2 : 1;
+    // k = max(1, (int)ceil(elite_fraction * M)) (controllers.cpp:164)
+    c->cem_k = std::max(1, (int)std::ceil(p.elite_fraction * (double)p.num_samples));
     c->m_begin = 0;
     long long m_end = c->M;
     if (p.shard_end > 0) {
@@ -675,6 +692,9 @@ smpc_status smpc_create(const smpc_problem* problem, smpc_ctx** out) {
     c->d_cand_off = dalloc<long long>((size_t)c->S * (c->n_w_blocks + 1));
     c->d_blk_part = dalloc<double>((size_t)c->S * c->n_u_blocks * TU);
     c->d_counters = dalloc<unsigned int>(16);
+    c->d_select = dalloc<SelectState>(1);
+    c->d_eq_cnt = dalloc<int>(c->n_w_blocks);
+    c->d_eq_off = dalloc<long long>(c->n_w_blocks + 1);
     c->d_gather1 = dalloc<double>((size_t)c->S * 2 * 8);
     c->d_gather2 = dalloc<double>((size_t)c->S * 2 * 8);
     c->d_gather3 = dalloc<double>((size_t)c->S * TU * 8);
@@ -752,7 +772,8 @@ void smpc_destroy(smpc_ctx* c) {
                   c->d_weights, c->d_blk_min, c->d_blk_eta, c->d_blk_part, c->d_gather1, c->d_gather2,
                   c->d_gather3, c->d_blk_arg, c->d_blk_nz, c->d_counters, c->d_costmap, c->d_result,
                   c->d_ro_x0, c->d_ro_mean, c->d_eps, c->d_outputs, c->d_wscratch, c->d_flags,
-                  c->d_cand, c->d_cand_cnt, c->d_cand_off};
+                  c->d_cand, c->d_cand_cnt, c->d_cand_off, c->d_select, c->d_eq_cnt, c->d_eq_off,
+                  c->d_dyn_tensor};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->h_result) cudaFreeHost(c->h_result);
@@ -1080,6 +1101,36 @@ smpc_status smpc_compute_weights(smpc_ctx* c, const double* costs, int64_t count
   });
 }
 
+smpc_status smpc_sorted_samples(smpc_ctx* c, int32_t system, int64_t count, int64_t* order_out, double* costs_out) {
+  if (!c || !order_out || system < 0 || system >= c->S || count < 1 || count > c->M_local) return SMPC_ERR_ARGUMENT;
+  return guarded(c, [&] {
+    if (c->world > 1 || c->M_local != c->M) throw ConfigError{"smpc_sorted_samples: single-shard contexts only"};
+    IterArgs a = c->base;
+    a.S = 1;
+    a.costs = c->d_costs + (size_t)system * c->M_local;
+    a.weights = c->d_weights + (size_t)system * c->M_local;
+    long long n_pad = 1;
+    while (n_pad < count) n_pad <<= 1;
+    unsigned long long* keys = dalloc<unsigned long long>((size_t)n_pad + 1);
+    long long* idx = dalloc<long long>((size_t)n_pad);
+    CK(launch_select(a, c->d_select, count, c->d_counters + 8, c->d_eq_cnt, c->d_eq_off, c->stream));
+    CK(launch_sort_selected(a, count, keys, idx, keys + n_pad, c->stream));
+    std::vector<unsigned long long> hk((size_t)count);
+    CK(cudaMemcpyAsync(order_out, idx, sizeof(long long) * count, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(hk.data(), keys, sizeof(unsigned long long) * count, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    cudaFree(keys);
+    cudaFree(idx);
+    if (costs_out) {
+      for (int64_t i = 0; i < count; ++i) {  // invert select.cu:cost_key
+        const unsigned long long k = hk[(size_t)i];
+        const unsigned long long b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+        memcpy(&costs_out[i], &b, sizeof b);
+      }
+    }
+  });
+}
+
 smpc_status smpc_set_x0(smpc_ctx* c, const float* x0) {
   if (!c || !x0) return SMPC_ERR_ARGUMENT;
   return guarded(c, [&] {
@@ -1112,6 +1163,7 @@ void* smpc_stream(smpc_ctx* c) { return c ? (void*)c->stream : nullptr; }
 
 int32_t smpc_kernels_per_solve(const smpc_ctx* c) {
   if (!c) return 0;
+  if (c->p.controller_kind == SMPC_CTRL_CEM) return 2 + c->I * (1 + 11 + 1);  // rollout, select (init+8+2), update
   return 2 + c->I * (3 + (c->world > 1 ? 1 : 0));
 }
 
@@ -1145,6 +1197,7 @@ smpc_status smpc_group_init(smpc_ctx** ctxs, int32_t n) {
   return guarded(ctxs[0], [&] {
     for (int r = 0; r < n; ++r) {
       smpc_ctx* c = ctxs[r];
+      if (n > 1 && c->p.controller_kind == SMPC_CTRL_CEM) throw ConfigError{"cem: multi-GPU sharding is not supported"};
       if (c->M != ctxs[0]->M || c->T != ctxs[0]->T || c->S != ctxs[0]->S || c->I != ctxs[0]->I)
         throw ConfigError{"smpc_group_init: contexts describe different problems"};
       c->rank = r;
@@ -1193,6 +1246,7 @@ smpc_status smpc_comm_init(smpc_ctx* c, const uint8_t id[128], int32_t rank, int
   if (!c || !id || world < 1 || rank < 0 || rank >= world || world > 8) return SMPC_ERR_ARGUMENT;
   return guarded(c, [&] {
     if (world == 1) return;
+    if (c->p.controller_kind == SMPC_CTRL_CEM) throw ConfigError{"cem: multi-GPU sharding is not supported"};
     NcclApi* api = nccl();
     if (!api) throw CudaError{"NCCL (libnccl.so.2) could not be loaded"};
     ncclUniqueId uid;

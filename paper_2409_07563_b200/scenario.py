@@ -19,11 +19,11 @@ import numpy as np
 
 SMPC_MAX_DIM = 16
 SMPC_MAX_PARAMS = 32
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 DYNAMICS_KINDS = {"unicycle": 0, "cartpole": 1, "diff_drive": 2, "double_integrator": 3}
 COST_KINDS = {"road": 0, "circle_track": 1, "diff_drive_nav": 2, "quadratic": 3}
-CONTROLLER_KINDS = {"mppi": 0, "dmd": 1, "tube": 3}
+CONTROLLER_KINDS = {"mppi": 0, "dmd": 1, "cem": 2, "tube": 3}
 
 # ModelDims per dynamics kind (dynamics.cpp:122-181) and state names
 # (used by initial_state, scenario.hpp:136-137 / state_from_named_values).
@@ -62,9 +62,12 @@ class SmpcProblem(ctypes.Structure):
         ("n_step_sizes", ctypes.c_int32),
         ("step_sizes", ctypes.POINTER(ctypes.c_float)),
         ("nominal_reset_bound", ctypes.c_double),
+        ("elite_fraction", ctypes.c_double),
         ("dynamics_kind", ctypes.c_int32),
         ("n_dyn_params", ctypes.c_int32),
         ("dyn_params", ctypes.c_double * SMPC_MAX_PARAMS),
+        ("dyn_tensor", ctypes.POINTER(ctypes.c_float)),
+        ("dyn_tensor_len", ctypes.c_int64),
         ("cost_kind", ctypes.c_int32),
         ("n_cost_params", ctypes.c_int32),
         ("cost_params", ctypes.c_double * SMPC_MAX_PARAMS),
@@ -194,6 +197,7 @@ class Scenario:
     step_size: float = 1.0
     step_size_per_step: Optional[Sequence[float]] = None
     nominal_reset_bound: float = math.inf
+    elite_fraction: float = 0.125
     initial_state: Dict[str, float] = dataclasses.field(default_factory=dict)
     device: int = 0
     # B200 deployment knob (not in the reference schema): weighted-update
@@ -281,6 +285,7 @@ class Scenario:
             p.n_step_sizes = len(steps)
             p.step_sizes = sarr.ctypes.data_as(ctypes.POINTER(ctypes.c_float))
         p.nominal_reset_bound = float(self.nominal_reset_bound)
+        p.elite_fraction = float(self.elite_fraction)
         p.dynamics_kind = DYNAMICS_KINDS[self.dynamics]
         dp = self._dyn_params()
         p.n_dyn_params = len(dp)
@@ -325,7 +330,8 @@ class Scenario:
                         "importance_sampling": self.importance_sampling},
             "dynamics": {"kind": self.dynamics, **self.dynamics_params},
             "cost": {"kind": self.cost, **self.cost_params},
-            "controller": {"kind": self.controller, "step_size": self.step_size},
+            "controller": {"kind": self.controller, "step_size": self.step_size,
+                           "elite_fraction": self.elite_fraction},
             "initial_state": self.initial_state,
         }
         if self.std_per_step:
