@@ -11,7 +11,7 @@ samples, T = 100 (the large-sample sweep config the metric is quoted on for
 with the WorkerPool chunk rule).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--workload di|cartpole|diffdrive] [--samples N] [--scaling strong|weak]
+                  [--workload di|cartpole|diffdrive|quadrotor] [--samples N] [--scaling strong|weak]
 
 Rank 0 prints ONE JSON line. `value` = samples/s of the whole job from
 device-resident graph replays (CUDA events on the context stream, L2 flushed
@@ -37,8 +37,13 @@ from paper_2409_07563_b200 import scenario as S  # noqa: E402
 
 # Algorithmic work per sample-step (reference-semantic
 # op counts; FP32 add/sub/mul/div/compare, noise generated in-kernel).
-FP32_OPS_PER_SAMPLE_STEP = {"di": 83, "cartpole": 56, "diffdrive": 90}
-FP64_OPS_PER_SAMPLE_STEP = {"di": 9, "cartpole": 23, "diffdrive": 19}
+# quadrotor (builder-defined): noise 4x29, control 4, clamp 8,
+# derivative 49, Euler 26, quaternion normalisation 11 (+1 sqrt); FP64:
+# quadratic cost 13x4 + total 1 + importance 4x3.
+FP32_OPS_PER_SAMPLE_STEP = {"di": 83, "cartpole": 56, "diffdrive": 90, "quadrotor": 214}
+FP64_OPS_PER_SAMPLE_STEP = {"di": 9, "cartpole": 23, "diffdrive": 19, "quadrotor": 65}
+# workloads whose model exists in the reference (oracle/_ref can time them)
+REFERENCE_WORKLOADS = ("di", "cartpole", "diffdrive")
 
 
 def make_scenario(workload: str, n: int) -> S.Scenario:
@@ -48,13 +53,16 @@ def make_scenario(workload: str, n: int) -> S.Scenario:
         return S.cartpole_scenario(num_samples=n, horizon=100, seed=1)
     if workload == "diffdrive":
         return S.diff_drive_nav_scenario(num_samples=n, horizon=56, seed=42)
+    if workload == "quadrotor":
+        return S.quadrotor_scenario(num_samples=n, horizon=100, seed=13)
     raise SystemExit(f"unknown workload {workload}")
 
 
 def workload_name(workload: str, n: int) -> str:
     return {"di": f"C5 double_integrator+circle_track MPPI N={n} T=100",
             "cartpole": f"C1 cartpole+quadratic MPPI N={n} T=100",
-            "diffdrive": f"C3 diff_drive+diff_drive_nav(costmap 110x110) MPPI N={n} T=56"}[workload]
+            "diffdrive": f"C3 diff_drive+diff_drive_nav(costmap 110x110) MPPI N={n} T=56",
+            "quadrotor": f"C2 quadrotor(13-state)+quadratic tracking MPPI N={n} T=100"}[workload]
 
 
 class ClockSampler:
@@ -175,7 +183,8 @@ def run_reference_arm(args):
     if rank != 0:
         return
     sc = make_scenario(args.workload, args.samples)
-    r = cpu_reference_run(sc, args.steps, args.warmup, budget_s=args.ref_budget)
+    r = cpu_reference_run(sc, args.steps, args.warmup, budget_s=args.ref_budget,
+                          prefer_ref=args.workload in REFERENCE_WORKLOADS)
     line = {
         "metric": "rollout samples/s per MPPI iteration (compute_control, I=1)",
         "value": r["value"], "unit": "samples/s", "n_gpus": world, "steps": r["n"], "warmup": args.warmup,
@@ -296,7 +305,8 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        r = cpu_reference_run(sc, steps=args.cpu_steps, warmup=1, budget_s=args.cpu_budget)
+        r = cpu_reference_run(sc, steps=args.cpu_steps, warmup=1, budget_s=args.cpu_budget,
+                              prefer_ref=args.workload in REFERENCE_WORKLOADS)
         cpu = {"value": r["value"], "unit": "samples/s", "cores": r["cores"], "kind": r["kind"],
                "ms_per_step": r["ms"],
                "sample": f"{r['n']} full-size compute_control solves (N={n_global}) after 1 warm-up"}
@@ -329,7 +339,7 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="di", choices=["di", "cartpole", "diffdrive"])
+    ap.add_argument("--workload", default="di", choices=["di", "cartpole", "diffdrive", "quadrotor"])
     ap.add_argument("--samples", type=int, default=1 << 20)
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
     ap.add_argument("--roofline-steps", type=int, default=20)

@@ -134,6 +134,9 @@ int oracle_dims_of(const smpc_problem* p, oracle_dims* d, oracle_error* err) {
     case SMPC_DYN_DOUBLE_INTEGRATOR:
       d->n_x = 4, d->n_u = 2, d->n_y = 4;
       return 0;
+    case SMPC_DYN_QUADROTOR:
+      d->n_x = 13, d->n_u = 4, d->n_y = 13;
+      return 0;
     default:
       return fail(err, "dynamics.kind is not recognized");
   }
@@ -144,6 +147,56 @@ static double dparam(const smpc_problem* p, int i, double dflt) {
 }
 static double cparam(const smpc_problem* p, int i, double dflt) {
   return i < p->n_cost_params ? p->cost_params[i] : dflt;
+}
+
+/* Builder-defined quadrotor (no reference counterpart; paper_2409_07563_b200/
+ * csrc/models.cuh:QuadrotorDyn is the device twin — parity unpinned by the
+ * reference). params {mass, gravity, tau, thrust_max, rate_max}. */
+typedef struct quad_params {
+  float inv_mass, gravity, inv_tau, hover, lo[4], hi[4];
+} quad_params;
+
+static quad_params quadrotor_params(const smpc_problem* p) {
+  quad_params q;
+  const float mass = (float)dparam(p, 0, 1.0), g = (float)dparam(p, 1, 9.81), tau = (float)dparam(p, 2, 0.05);
+  const float tmax = (float)dparam(p, 3, 39.24), rmax = (float)dparam(p, 4, 5.0);
+  q.inv_mass = 1.0f / mass;
+  q.inv_tau = 1.0f / tau;
+  q.gravity = g;
+  q.hover = mass * g;
+  for (int i = 0; i < 3; ++i) q.lo[i] = -rmax, q.hi[i] = rmax;
+  q.lo[3] = -q.hover;
+  q.hi[3] = tmax - q.hover;
+  return q;
+}
+
+static void quadrotor_derivative(const smpc_problem* p, const float* x, const float* u, float* dx) {
+  const quad_params q = quadrotor_params(p);
+  const float qw = x[6], qx = x[7], qy = x[8], qz = x[9];
+  const float wx = x[10], wy = x[11], wz = x[12];
+  const float acc = (q.hover + u[3]) * q.inv_mass;
+  const float zx = 2.0f * (qx * qz + qw * qy);
+  const float zy = 2.0f * (qy * qz - qw * qx);
+  const float zz = 1.0f - 2.0f * (qx * qx + qy * qy);
+  dx[0] = x[3];
+  dx[1] = x[4];
+  dx[2] = x[5];
+  dx[3] = acc * zx;
+  dx[4] = acc * zy;
+  dx[5] = acc * zz - q.gravity;
+  dx[6] = -0.5f * (qx * wx + qy * wy + qz * wz);
+  dx[7] = 0.5f * (qw * wx + qy * wz - qz * wy);
+  dx[8] = 0.5f * (qw * wy - qx * wz + qz * wx);
+  dx[9] = 0.5f * (qw * wz + qx * wy - qy * wx);
+  dx[10] = (u[0] - wx) * q.inv_tau;
+  dx[11] = (u[1] - wy) * q.inv_tau;
+  dx[12] = (u[2] - wz) * q.inv_tau;
+}
+
+/* quaternion re-normalisation after the Euler step */
+static void quadrotor_post_step(float* x) {
+  const float n = sqrtf(x[6] * x[6] + x[7] * x[7] + x[8] * x[8] + x[9] * x[9]);
+  for (int i = 6; i < 10; ++i) x[i] = x[i] / n;
 }
 
 /* state_derivative overrides: unicycle dynamics.cpp:127-131, cartpole :143-156,
@@ -176,6 +229,9 @@ static void state_derivative(const smpc_problem* p, const float* x, const float*
       dx[2] = u[0];
       dx[3] = u[1];
       break;
+    case SMPC_DYN_QUADROTOR:
+      quadrotor_derivative(p, x, u, dx);
+      break;
   }
 }
 
@@ -190,11 +246,19 @@ static void clamp_control(const smpc_problem* p, const float* u, float* out, int
     }
     return;
   }
+  if (p->dynamics_kind == SMPC_DYN_QUADROTOR) {
+    const quad_params q = quadrotor_params(p);
+    for (int i = 0; i < 4; ++i) {
+      const float a = u[i] < q.lo[i] ? q.lo[i] : u[i];
+      out[i] = q.hi[i] < a ? q.hi[i] : a;
+    }
+    return;
+  }
   for (int i = 0; i < n_u; ++i) out[i] = u[i];
 }
 
 static int angular_channel(const smpc_problem* p) {
-  return p->dynamics_kind == SMPC_DYN_DOUBLE_INTEGRATOR ? -1 : 2;
+  return (p->dynamics_kind == SMPC_DYN_DOUBLE_INTEGRATOR || p->dynamics_kind == SMPC_DYN_QUADROTOR) ? -1 : 2;
 }
 
 /* step_raw (dynamics.cpp:45-54) with the default observe (:41-43). */
@@ -204,6 +268,7 @@ static void step_raw(const smpc_problem* p, const oracle_dims* d, const float* x
   clamp_control(p, u, u_c, d->n_u);
   state_derivative(p, x, u_c, dx);
   for (int i = 0; i < d->n_x; ++i) x_next[i] = x[i] + dt * dx[i];
+  if (p->dynamics_kind == SMPC_DYN_QUADROTOR) quadrotor_post_step(x_next);
   const int ang = angular_channel(p);
   if (ang >= 0) x_next[ang] = wrap_angle(x_next[ang]);
   for (int i = 0; i < d->n_y; ++i) y[i] = x_next[i];

@@ -155,6 +155,7 @@ ModelOps ops_unicycle(bool fma_libm);
 ModelOps ops_cartpole(bool fma_libm);
 ModelOps ops_diff_drive(bool fma_libm);
 ModelOps ops_double_integrator();
+ModelOps ops_quadrotor();
 
 cudaError_t launch_select(const IterArgs& a, SelectState* st, long long k, unsigned int* counters, int* eq_cnt,
                           long long* eq_off, cudaStream_t stream);

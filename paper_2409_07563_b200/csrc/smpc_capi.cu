@@ -218,6 +218,13 @@ void validate(smpc_ctx* c) {
       c->ops = ops_diff_drive(c->fma);
       break;
     case SMPC_DYN_DOUBLE_INTEGRATOR: c->ops = ops_double_integrator(); break;
+    case SMPC_DYN_QUADROTOR:  // builder-defined (models.cuh:QuadrotorDyn)
+      if (!((float)pd(p, 0, 1.0) > 0.0f) || !((float)pd(p, 2, 0.05) > 0.0f))
+        throw RuntimeError{"quadrotor: mass and rate time constant must be > 0"};
+      if (!((float)pd(p, 3, 39.24) > (float)pd(p, 0, 1.0) * (float)pd(p, 1, 9.81)) || !((float)pd(p, 4, 5.0) > 0.0f))
+        throw RuntimeError{"quadrotor: thrust_max must exceed hover thrust and rate_max must be > 0"};
+      c->ops = ops_quadrotor();
+      break;
     default: throw ConfigError{"dynamics.kind is not recognized"};
   }
   c->nx = c->ops.nx, c->nu = c->ops.nu, c->ny = c->ops.ny;
@@ -256,7 +263,7 @@ void validate(smpc_ctx* c) {
       break;
     default: throw ConfigError{"cost.kind is not recognized"};
   }
-  static const char* dyn_names[] = {"unicycle", "cartpole", "diff_drive", "double_integrator"};
+  static const char* dyn_names[] = {"unicycle", "cartpole", "diff_drive", "double_integrator", "quadrotor", "mlp"};
   if (cost_ny != c->ny)
     throw ConfigError{"cost '" + cost_name + "' expects " + std::to_string(cost_ny) +
                       " output channels but model '" + dyn_names[p.dynamics_kind] + "' produces " +
@@ -376,8 +383,14 @@ void fill_args(smpc_ctx* c) {
       for (int i = 0; i < 6; ++i) a.dyn.p[i] = (float)pd(p, i, d[i]);
       break;
     }
+    case SMPC_DYN_QUADROTOR: {
+      const double d[5] = {1.0, 9.81, 0.05, 39.24, 5.0};
+      for (int i = 0; i < 5; ++i) a.dyn.p[i] = (float)pd(p, i, d[i]);
+      break;
+    }
     default: break;
   }
+  a.dyn.tensor = c->d_dyn_tensor;
   CostParams& cp = a.cost;
   memset(&cp, 0, sizeof(cp));
   switch (p.cost_kind) {

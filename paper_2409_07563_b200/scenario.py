@@ -21,7 +21,9 @@ SMPC_MAX_DIM = 16
 SMPC_MAX_PARAMS = 32
 ABI_VERSION = 2
 
-DYNAMICS_KINDS = {"unicycle": 0, "cartpole": 1, "diff_drive": 2, "double_integrator": 3}
+DYNAMICS_KINDS = {"unicycle": 0, "cartpole": 1, "diff_drive": 2, "double_integrator": 3,
+                  # builder-defined (no reference counterpart): BASELINE.json configs[1] / configs[3]
+                  "quadrotor": 4, "mlp": 5}
 COST_KINDS = {"road": 0, "circle_track": 1, "diff_drive_nav": 2, "quadratic": 3}
 CONTROLLER_KINDS = {"mppi": 0, "dmd": 1, "cem": 2, "tube": 3}
 
@@ -32,12 +34,18 @@ MODEL_DIMS = {
     "cartpole": (4, 1, 4),
     "diff_drive": (3, 2, 3),
     "double_integrator": (4, 2, 4),
+    "quadrotor": (13, 4, 13),
+    "mlp": (7, 2, 7),
 }
 STATE_NAMES = {
     "unicycle": ["X", "Y", "YAW"],
     "cartpole": ["X", "X_DOT", "THETA", "THETA_DOT"],
     "diff_drive": ["X", "Y", "YAW"],
     "double_integrator": ["X", "Y", "V_X", "V_Y"],
+    "quadrotor": ["X", "Y", "Z", "V_X", "V_Y", "V_Z", "QW", "QX", "QY", "QZ", "W_X", "W_Y", "W_Z"],
+    # AutoRally state convention (MPPI-Generic AutoRallyDynamics): pose, then the
+    # body-frame dynamic state the network predicts
+    "mlp": ["X", "Y", "YAW", "ROLL", "V_X", "V_Y", "YAW_RATE"],
 }
 
 
@@ -231,6 +239,9 @@ class Scenario:
         if self.dynamics == "diff_drive":
             return [d.get("wheel_radius", 1.0), d.get("wheel_length", 1.0), d.get("v_min", -0.35),
                     d.get("v_max", 0.5), d.get("w_min", -0.5), d.get("w_max", 0.5)]
+        if self.dynamics == "quadrotor":
+            return [d.get("mass", 1.0), d.get("gravity", 9.81), d.get("rate_time_constant", 0.05),
+                    d.get("thrust_max", 39.24), d.get("rate_max", 5.0)]
         return []
 
     def _cost_params(self) -> List[float]:
@@ -363,6 +374,18 @@ def di_swarm_scenario(num_samples: int = 1 << 20, horizon: int = 100, seed: int 
     return Scenario(num_samples=num_samples, horizon=horizon, dt=0.02, lambda_=1.0, control_std=(1.0, 1.0),
                     rng_seed=seed, importance_sampling=False, dynamics="double_integrator",
                     cost="circle_track", initial_state={"X": 2.0, "V_Y": 2.0})
+
+
+def quadrotor_scenario(num_samples: int = 8192, horizon: int = 100, seed: int = 13) -> Scenario:
+    """C2: 13-state quadrotor, quadratic tracking of the hover point (1, 1, 1)
+    from hover at the origin (BASELINE.json configs[1]; builder-defined model,
+    see models.cuh:QuadrotorDyn). Control = (body-rate commands, thrust offset
+    from hover), so the zero mean is hover."""
+    target = [1.0, 1.0, 1.0, 0.0, 0.0, 0.0, 1.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0]
+    weights = [10.0, 10.0, 10.0, 1.0, 1.0, 1.0, 5.0, 5.0, 5.0, 5.0, 0.1, 0.1, 0.1]
+    return Scenario(num_samples=num_samples, horizon=horizon, dt=0.02, lambda_=1.0,
+                    control_std=(0.5, 0.5, 0.5, 2.0), rng_seed=seed, dynamics="quadrotor", cost="quadratic",
+                    target=target, weights=weights, initial_state={"QW": 1.0})
 
 
 def synthetic_costmap(seed: int = 3) -> Costmap:

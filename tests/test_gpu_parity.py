@@ -46,6 +46,8 @@ def scenarios(S):
         "di_quadratic_dmd": sp(num_samples=384, horizon=25, dynamics="double_integrator", cost="quadratic",
                                target=[1.0, -1.0, 0.0, 0.0], weights=[1.0, 1.0, 0.1, 0.1], rng_seed=3,
                                control_std=(0.7, 0.4), controller="dmd", step_size=0.6, lambda_=2.0),
+        # BASELINE.json configs[1]: builder-defined 13-state quadrotor (restated oracle only)
+        "quadrotor": S.quadrotor_scenario(num_samples=1024, horizon=100, seed=13),
     }
 
 
@@ -81,7 +83,7 @@ def test_icdf_whole_domain_bit_exact(mods):
 
 
 @pytest.mark.parametrize("name", ["cartpole", "double_integrator", "diff_drive_nav", "unicycle_road",
-                                  "cartpole_road_perstep", "di_quadratic_dmd"])
+                                  "cartpole_road_perstep", "di_quadratic_dmd", "quadrotor"])
 def test_generate_samples_bit_exact(mods, name):
     sc = scenarios(mods["S"])[name]
     n_x, n_u, n_y = sc.dims
@@ -94,7 +96,7 @@ def test_generate_samples_bit_exact(mods, name):
 
 
 @pytest.mark.parametrize("name", ["cartpole", "double_integrator", "diff_drive_nav", "unicycle_road",
-                                  "cartpole_road_perstep", "di_quadratic_dmd"])
+                                  "cartpole_road_perstep", "di_quadratic_dmd", "quadrotor"])
 @pytest.mark.parametrize("systems", [1, 2])
 def test_rollout_costs_bit_exact(mods, name, systems):
     """Fused rollout (Philox regenerated in-kernel and injected noise) vs oracle:
@@ -136,7 +138,7 @@ def test_compute_weights_matches_oracle(mods):
 
 
 @pytest.mark.parametrize("name", ["cartpole", "double_integrator", "diff_drive_nav", "unicycle_road",
-                                  "cartpole_road_perstep", "di_quadratic_dmd"])
+                                  "cartpole_road_perstep", "di_quadratic_dmd", "quadrotor"])
 def test_compute_control_matches_oracle(mods, name):
     """Three warm-started solves: rho and argmin exact, U*/states/weights within 1e-4."""
     sc = scenarios(mods["S"])[name]

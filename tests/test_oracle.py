@@ -201,3 +201,22 @@ def test_port_vs_reference_randomized(oracle_built):
         c1 = P.rollout(sc, x0, mean[None], e1)
         c2 = R.rollout(sc, x0, mean[None], e1, strategy=int(rng.integers(0, 2)), workers=3)
         assert np.array_equal(c1.view(np.uint64), c2.view(np.uint64))
+
+
+def test_quadrotor_hover_is_an_equilibrium(port):
+    """Builder-defined quadrotor (no reference model): zero control from hover
+    keeps the state exactly (thrust m g cancels gravity, unit quaternion)."""
+    sc = S.quadrotor_scenario(num_samples=4, horizon=5)
+    x = sc.x0()
+    assert x[6] == 1.0
+    xn, y = port.step(sc, x, np.zeros(4, np.float32), np.float32(0.02))
+    assert np.array_equal(xn, x) and np.array_equal(y, x)
+    # a pure yaw-rate command rotates about z, keeps |q| = 1 and does not lift
+    xr = x.copy()
+    for _ in range(50):
+        xr, _ = port.step(sc, xr, np.array([0, 0, 1.0, 0], np.float32), np.float32(0.02))
+    assert abs(float(np.linalg.norm(xr[6:10])) - 1.0) < 1e-6
+    assert abs(xr[2]) < 1e-5 and xr[12] > 0.9
+    # thrust is clamped to [0, T_max]
+    xc, _ = port.step(sc, x, np.array([0, 0, 0, 1e6], np.float32), np.float32(0.02))
+    assert abs(xc[5] - 0.02 * (39.24 - 9.81)) < 1e-5
