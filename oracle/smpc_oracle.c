@@ -137,6 +137,10 @@ int oracle_dims_of(const smpc_problem* p, oracle_dims* d, oracle_error* err) {
     case SMPC_DYN_QUADROTOR:
       d->n_x = 13, d->n_u = 4, d->n_y = 13;
       return 0;
+    case SMPC_DYN_MLP:
+      if (!p->dyn_tensor || p->dyn_tensor_len != 1412) return fail(err, "mlp: dyn_tensor must hold 1412 floats");
+      d->n_x = 7, d->n_u = 2, d->n_y = 7;
+      return 0;
     default:
       return fail(err, "dynamics.kind is not recognized");
   }
@@ -199,6 +203,36 @@ static void quadrotor_post_step(float* x) {
   for (int i = 6; i < 10; ++i) x[i] = x[i] / n;
 }
 
+/* Builder-defined AutoRally-style neural dynamics (device twin: csrc/models.cuh
+ * MlpDyn + csrc/mlp.cu; parity is tolerance-based: the device runs layer 2 in
+ * 3xTF32 on the tensor cores and uses an exp-based tanh). Blob layout
+ * W1[32][6] b1[32] W2[32][32] b2[32] W3[4][32] b3[4]. */
+static void mlp_derivative(const smpc_problem* p, const float* x, const float* u, float* dx) {
+  const float* w = p->dyn_tensor;
+  const float *W1 = w, *b1 = W1 + 192, *W2 = b1 + 32, *b2 = W2 + 1024, *W3 = b2 + 32, *b3 = W3 + 128;
+  const float in[6] = {x[3], x[4], x[5], x[6], u[0], u[1]};
+  float h1[32], h2[32];
+  for (int j = 0; j < 32; ++j) {
+    float acc = b1[j];
+    for (int k = 0; k < 6; ++k) acc += W1[j * 6 + k] * in[k];
+    h1[j] = tanhf(acc);
+  }
+  for (int j = 0; j < 32; ++j) {
+    float acc = b2[j];
+    for (int k = 0; k < 32; ++k) acc += W2[j * 32 + k] * h1[k];
+    h2[j] = tanhf(acc);
+  }
+  const float c = cosf(x[2]), s = sinf(x[2]);
+  dx[0] = x[4] * c - x[5] * s;
+  dx[1] = x[4] * s + x[5] * c;
+  dx[2] = x[6];
+  for (int q = 0; q < 4; ++q) {
+    float acc = b3[q];
+    for (int j = 0; j < 32; ++j) acc += W3[q * 32 + j] * h2[j];
+    dx[3 + q] = acc;
+  }
+}
+
 /* state_derivative overrides: unicycle dynamics.cpp:127-131, cartpole :143-156,
  * diff-drive :167-171, double integrator :176-181. */
 static void state_derivative(const smpc_problem* p, const float* x, const float* u, float* dx) {
@@ -232,6 +266,9 @@ static void state_derivative(const smpc_problem* p, const float* x, const float*
     case SMPC_DYN_QUADROTOR:
       quadrotor_derivative(p, x, u, dx);
       break;
+    case SMPC_DYN_MLP:
+      mlp_derivative(p, x, u, dx);
+      break;
   }
 }
 
@@ -243,6 +280,13 @@ static void clamp_control(const smpc_problem* p, const float* u, float* out, int
     for (int i = 0; i < 2; ++i) {
       const float a = u[i] < lo[i] ? lo[i] : u[i]; /* std::max(u, lo) */
       out[i] = hi[i] < a ? hi[i] : a;              /* std::min(., hi) */
+    }
+    return;
+  }
+  if (p->dynamics_kind == SMPC_DYN_MLP) { /* steering, throttle in [-1, 1] */
+    for (int i = 0; i < 2; ++i) {
+      const float a = u[i] < -1.0f ? -1.0f : u[i];
+      out[i] = 1.0f < a ? 1.0f : a;
     }
     return;
   }

@@ -12,6 +12,15 @@ constexpr int kMaxNX = 16;
 constexpr int kMaxNU = 4;
 constexpr int kMaxNY = 16;
 constexpr int kRolloutThreads = 128;
+
+// SMPC_DYN_MLP parameter blob (smpc_b200.h): W1[32][6] b1[32] W2[32][32]
+// b2[32] W3[4][32] b3[4], fp32 row-major.
+namespace mlp_layout {
+constexpr int IN = 6, HID = 32, OUT = 4;
+constexpr int W1 = 0, B1 = W1 + HID * IN, W2 = B1 + HID, B2 = W2 + HID * HID, W3 = B2 + HID, B3 = W3 + OUT * HID;
+constexpr int TOTAL = B3 + OUT;  // 1412
+}  // namespace mlp_layout
+
 constexpr int kUpdateThreads = 256;
 constexpr int kUpdateWarps = kUpdateThreads / 32;
 
@@ -156,6 +165,7 @@ ModelOps ops_cartpole(bool fma_libm);
 ModelOps ops_diff_drive(bool fma_libm);
 ModelOps ops_double_integrator();
 ModelOps ops_quadrotor();
+ModelOps ops_mlp(bool fma_libm);
 
 cudaError_t launch_select(const IterArgs& a, SelectState* st, long long k, unsigned int* counters, int* eq_cnt,
                           long long* eq_off, cudaStream_t stream);

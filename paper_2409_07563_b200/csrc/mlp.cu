@@ -1,0 +1,393 @@
+// Neural-network (AutoRally-style MLP) dynamics rollout on the 5th-generation
+// tensor cores (BASELINE.json configs[3]; builder-defined model, see
+// models.cuh:MlpDyn — no reference counterpart, tolerance parity against the
+// restated oracle oracle/smpc_oracle.c:mlp_derivative).
+//
+// One CTA = 128 samples of one system (one tcgen05 M=128 tile; grid.y =
+// system, so Tube's nominal and real rollouts are separate CTAs that
+// regenerate the same Philox draw — cheaper than doubling the per-thread
+// state). Per timestep:
+//
+//   SIMT   u = clamp(mean + eps); h1 = tanh(W1 [roll,vx,vy,r,u] + b1)    (6x32)
+//          h1 -> shared memory as TF32 hi/lo pairs in the UMMA K-major
+//          no-swizzle core-matrix layout (row = sample)
+//   tcgen05 D[s] (TMEM, 128 lanes x 32 fp32 columns) = H1 W2^T in 3xTF32:
+//          hi*hi + hi*lo + lo*hi, 4 K-steps of 8 -> 12 MMAs per system,
+//          issued by one thread, completion via tcgen05.commit -> mbarrier
+//   SIMT   tcgen05.ld (32x32b.x32: thread = TMEM lane = sample row) ->
+//          h2 = tanh(D + b2) -> (roll,vx,vy,r)' = W3 h2 + b3 (32x4) ->
+//          kinematics -> explicit Euler -> wrap yaw -> running cost
+//
+// Layer 2 (32x32, 76% of the MACs) is the dense batched contraction the
+// tensor cores take; layers 1 and 3 stay in registers (K = 6 and N = 4 are
+// below a tcgen05 tile and need no round trip). The costs, argmin reduction,
+// weights, update and nominal rollout are the shared MPPI kernels
+// (kernels.cuh), so MPPI, DMD, CEM and Tube all run on this rollout.
+#include <cuda_runtime.h>
+
+#include "inst_common.cuh"
+
+namespace smpc_dev {
+namespace mlpk {
+
+using namespace mlp_layout;
+
+// Instruction descriptor, kind::tf32: D fp32 (bits 4-5 = 1), A/B TF32
+// (bits 7-9 = 2, 10-12 = 2), both K-major, N = 32 (bits 17-22 = N>>3),
+// M = 128 (bits 24-28 = M>>4).
+constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((32u >> 3) << 17) | ((128u >> 4) << 24);
+constexpr int kTile = 128;                      // samples per CTA (= M)
+constexpr int kHBytes = kTile * HID * 4;        // one TF32 operand tile [128 x 32]
+constexpr int kWBytes = HID * HID * 4;          // W2 operand tile [32 x 32]
+constexpr uint32_t kLBO = 128;                  // next 4-element K chunk
+constexpr uint32_t kSBO = HID * 32;             // next 8-row group (K = 32: 8 chunks x 128 B)
+
+// Byte offset of element (r, k) in a K-major SWIZZLE_NONE tile with HID columns:
+// core matrices of 8 rows x 16 B, K chunks LBO apart, row groups SBO apart.
+__device__ __forceinline__ uint32_t core_off(int r, int k) {
+  return (uint32_t)((r >> 3) * kSBO + (k >> 2) * kLBO + (r & 7) * 16 + (k & 3) * 4);
+}
+
+// UMMA shared-memory matrix descriptor (sm_100): start >> 4 [0,14), LBO >> 4
+// [16,30), SBO >> 4 [32,46), version 1 [46,48), base offset 0, layout 0 =
+// SWIZZLE_NONE [61,64).
+__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr) {
+  return (uint64_t)((saddr & 0x3FFFFu) >> 4) | ((uint64_t)(kLBO >> 4) << 16) | ((uint64_t)(kSBO >> 4) << 32) |
+         (1ull << 46);
+}
+
+__device__ __forceinline__ float to_tf32(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(kIdesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+  asm volatile("fence.mbarrier_init.release.cluster;");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(bar)),
+      "r"(parity));
+}
+
+// 32 consecutive fp32 TMEM columns of this thread's lane.
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+}
+
+// Shared-memory carve-up (bytes); host and device agree through this struct.
+struct Smem {
+  int w2hi, w2lo, h0, params, sig2, sigma, mean, bar, total;
+  __host__ __device__ Smem(int S, int TU) {
+    w2hi = 0;
+    w2lo = w2hi + kWBytes;
+    h0 = w2lo + kWBytes;                        // [hi|lo][128 x 32]
+    params = h0 + 2 * kHBytes;                  // W1 b1 b2 W3 b3 (fp32)
+    sig2 = (params + (TOTAL - HID * HID) * 4 + 15) / 16 * 16;
+    sigma = sig2 + TU * 8;
+    mean = sigma + TU * 4;
+    bar = (mean + S * TU * 4 + 15) / 16 * 16;   // mbarrier (8 B) + TMEM base (4 B); mean = all S systems
+    total = bar + 16;
+  }
+};
+
+template <class Dyn, class Cost, bool INJ, bool IMP>
+__global__ void __launch_bounds__(kTile, 4) mlp_rollout_kernel(const IterArgs a, const Dyn dyn, Cost cost) {
+  constexpr int NU = 2, NX = 7, NY = 7;
+  const int S = a.S, sys = blockIdx.y;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  if (aborted(a)) return;
+  const int T = a.T, TU = T * NU;
+  const Smem L(S, TU);
+  float* prm = reinterpret_cast<float*>(smem + L.params);  // W1 [0,192) b1 [192,224) b2 [224,256) W3 [256,384) b3 [384,388)
+  const float* sW1 = prm;
+  const float* sB1 = prm + HID * IN;
+  const float* sB2 = sB1 + HID;
+  const float* sW3 = sB2 + HID;
+  const float* sB3 = sW3 + OUT * HID;
+  double* sig2_s = reinterpret_cast<double*>(smem + L.sig2);
+  float* sigma_s = reinterpret_cast<float*>(smem + L.sigma);
+  float* mean_s = reinterpret_cast<float*>(smem + L.mean);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L.bar);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L.bar + 8);
+  const int tid = threadIdx.x, warp = tid >> 5;
+
+  // ---- one-time staging: W2 as TF32 hi/lo operand tiles, the SIMT layers, sampler tables
+  const float* w = dyn.w;
+  for (int e = tid; e < HID * HID; e += kTile) {
+    const int n = e / HID, k = e % HID;  // W2[n][k]: B operand row n (output unit), K-major
+    const float v = __ldg(w + W2 + e);
+    const float hi = to_tf32(v);
+    *reinterpret_cast<float*>(smem + L.w2hi + core_off(n, k)) = hi;
+    *reinterpret_cast<float*>(smem + L.w2lo + core_off(n, k)) = to_tf32(v - hi);
+  }
+  for (int e = tid; e < HID * IN + HID; e += kTile) prm[e] = __ldg(w + W1 + e);         // W1, b1
+  for (int e = tid; e < HID; e += kTile) prm[HID * IN + HID + e] = __ldg(w + B2 + e);  // b2
+  for (int e = tid; e < OUT * HID + OUT; e += kTile) prm[HID * IN + 2 * HID + e] = __ldg(w + W3 + e);  // W3, b3
+  for (int k = tid; k < TU; k += kTile) {
+    sigma_s[k] = a.sigma[k];
+    if (IMP) sig2_s[k] = a.sig2[k];
+  }
+  for (int k = tid; k < S * TU; k += kTile) mean_s[k] = a.mean_in[k];
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "n"(32));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) mbar_init(bar, 1);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  const int i = blockIdx.x * kTile + tid;
+  const bool active = i < a.M_local;
+  const long long m = a.m_begin + i;
+  const bool is_mean = a.with_mean && m == 0;
+  const bool zero_mean = m >= a.zero_begin;
+  const uint32_t stream = noise_stream(a);
+
+  float x[NX], y[NY];
+  double total = 0.0, imp = 0.0;
+#pragma unroll
+  for (int c = 0; c < NX; ++c) x[c] = a.x0[sys * NX + c];
+  unsigned long long err = kNoError;
+  float4 zq = make_float4(0.f, 0.f, 0.f, 0.f);
+  uint32_t phase = 0;
+  unsigned char* hhi = smem + L.h0;
+  unsigned char* hlo = hhi + kHBytes;
+  const float* mean_sys = mean_s + sys * TU;  // u = mean_s + eps; eps drawn about system 0's mean
+
+  for (int t = 0; t < T; ++t) {
+    // ---- noise (sampling.cpp:64-88) and the sampled, clamped control
+    float u[NU], uc[NU];
+#pragma unroll
+    for (int c = 0; c < NU; ++c) {
+      const int k = t * NU + c;
+      float e;
+      if constexpr (INJ) {
+        e = active ? a.eps_in[(size_t)i * TU + k] : 0.0f;
+      } else {
+        if ((k & 3) == 0) zq = normal_quad_fast(a, stream, (uint32_t)m, (uint32_t)(k >> 2));
+        float ev = F_MUL(sigma_s[k], quad_lane(zq, k & 3));
+        if (zero_mean) ev = F_SUB(ev, mean_s[k]);
+        e = is_mean ? 0.0f : ev;
+      }
+      const float mu = mean_sys[k];
+      u[c] = F_ADD(mu, e);
+      if constexpr (IMP) imp = D_ADD(imp, __ddiv_rn(D_MUL((double)mu, (double)e), sig2_s[k]));
+    }
+    dyn.clamp_control(u, uc);
+    // ---- layer 1 (SIMT) -> this sample's row of the hi/lo A operand
+    const float in[IN] = {x[3], x[4], x[5], x[6], uc[0], uc[1]};
+#pragma unroll
+    for (int j0 = 0; j0 < HID; j0 += 4) {
+      float hv[4], lv[4];
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) {
+        const int j = j0 + jj;
+        float acc = sB1[j];
+#pragma unroll
+        for (int k = 0; k < IN; ++k) acc += sW1[j * IN + k] * in[k];
+        const float h = mlp_tanh(acc);
+        hv[jj] = to_tf32(h);
+        lv[jj] = to_tf32(h - hv[jj]);
+      }
+      *reinterpret_cast<float4*>(hhi + core_off(tid, j0)) = make_float4(hv[0], hv[1], hv[2], hv[3]);
+      *reinterpret_cast<float4*>(hlo + core_off(tid, j0)) = make_float4(lv[0], lv[1], lv[2], lv[3]);
+    }
+    // ---- layer 2 on the tensor cores: D = H1 W2^T (3xTF32), one issuing thread
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy smem writes -> async proxy
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (tid == 0) {
+      const uint32_t ahi = smem_u32(hhi), alo = ahi + kHBytes;
+      const uint32_t bhi = smem_u32(smem + L.w2hi), blo = smem_u32(smem + L.w2lo);
+#pragma unroll
+      for (int kk = 0; kk < HID / 8; ++kk) {  // K-step of 8 TF32 = 2 core-matrix chunks = 256 B
+        const uint32_t off = (uint32_t)kk * 2u * kLBO;
+        mma_tf32(tmem, smem_desc(ahi + off), smem_desc(bhi + off), kk > 0 ? 1u : 0u);
+        mma_tf32(tmem, smem_desc(ahi + off), smem_desc(blo + off), 1u);
+        mma_tf32(tmem, smem_desc(alo + off), smem_desc(bhi + off), 1u);
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                   : "memory");
+    }
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+
+    // ---- epilogue: layer 3 + kinematics + Euler + running cost
+    float d2[HID];
+    tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16), d2);
+    float o[OUT];
+#pragma unroll
+    for (int q = 0; q < OUT; ++q) o[q] = sB3[q];
+#pragma unroll
+    for (int j = 0; j < HID; ++j) {
+      const float h2 = mlp_tanh(d2[j] + sB2[j]);
+#pragma unroll
+      for (int q = 0; q < OUT; ++q) o[q] += sW3[q * HID + j] * h2;
+    }
+    float dx[NX];
+    dyn.kinematics(x, dx);
+#pragma unroll
+    for (int q = 0; q < OUT; ++q) dx[3 + q] = o[q];
+    float xn[NX];
+#pragma unroll
+    for (int c = 0; c < NX; ++c) xn[c] = F_ADD(x[c], F_MUL(a.dt, dx[c]));
+    xn[2] = wrap_angle(xn[2]);
+#pragma unroll
+    for (int c = 0; c < NY; ++c) y[c] = xn[c];
+    const double ct = cost.running_cost(y, uc, t);
+    if (active && err == kNoError) {  // engine.cpp:51-65, first failure per sample
+      int ch = -1;
+#pragma unroll
+      for (int c = NX - 1; c >= 0; --c)
+        if (!isfinite(xn[c])) ch = c;
+      if (ch >= 0) err = make_error_key(0, sys, m, t, 0, ch);
+      else if (!(ct >= 0.0 && ct <= DBL_MAX)) err = make_error_key(0, sys, m, t, 1, 0);
+    }
+    total = D_ADD(total, ct);
+    if (a.outputs && active) {
+      float* op = a.outputs + (((size_t)sys * a.M_local + i) * T + t) * NY;
+#pragma unroll
+      for (int c = 0; c < NY; ++c) op[c] = y[c];
+    }
+#pragma unroll
+    for (int c = 0; c < NX; ++c) x[c] = xn[c];
+  }
+
+  // ---- release TMEM (the allocating warp), then totals (engine.cpp:236-238, :263-265)
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(32));
+  }
+  double J = INFINITY;
+  if (active) {
+    if (err == kNoError) {
+      const double term = cost.terminal_cost(y);
+      if (!(term >= 0.0 && term <= DBL_MAX)) err = make_error_key(0, sys, m, T - 1, 2, 0);
+      J = D_ADD(total, term);
+      if constexpr (IMP) J = D_ADD(J, D_MUL(a.lambda, imp));
+      if (!isfinite(J) && err == kNoError) err = make_error_key(1, sys, m, 0, 0, 0);
+    } else {
+      J = NAN;
+    }
+    a.costs[(size_t)sys * a.M_local + i] = J;
+  }
+  if (err != kNoError) atomicMin(&a.header->err_key, err);
+
+  // ---- block (min, argmin) of this system; the last CTA of the whole grid
+  // reduces every system (same output as publish_block_min, 2-D grid).
+  {
+    double j = active ? J : INFINITY;
+    if (!(j == j)) j = INFINITY;
+    long long mm = active ? m : LLONG_MAX;
+    block_argmin<kTile>(j, mm);
+    if (tid == 0) {
+      a.blk_min[sys * a.n_roll_blocks + blockIdx.x] = j;
+      a.blk_arg[sys * a.n_roll_blocks + blockIdx.x] = mm;
+    }
+  }
+  if (!last_block_done(&a.counters[0], gridDim.x * gridDim.y)) return;
+  for (int s = 0; s < S; ++s) {
+    double j = INFINITY;
+    long long mm = LLONG_MAX;
+    for (int b = tid; b < a.n_roll_blocks; b += kTile) {
+      const double j2 = ((volatile double*)a.blk_min)[s * a.n_roll_blocks + b];
+      const long long m2 = ((volatile long long*)a.blk_arg)[s * a.n_roll_blocks + b];
+      if (better(j2, m2, j, mm)) j = j2, mm = m2;
+    }
+    block_argmin<kTile>(j, mm);
+    if (tid == 0) {
+      double* g = a.gather1 + ((size_t)a.rank * a.S + s) * 2;
+      g[0] = j;
+      g[1] = __longlong_as_double(mm);
+    }
+  }
+}
+
+template <class Dyn, class Cost>
+cudaError_t launch(const IterArgs& a, const Dyn& dyn, const Cost& cost, cudaStream_t st) {
+  const Smem L(a.S, a.T * 2);
+  const size_t smem = (size_t)L.total;
+  const dim3 grid((unsigned)((a.M_local + kTile - 1) / kTile), (unsigned)a.S), block(kTile);
+  auto k = mlp_rollout_kernel<Dyn, Cost, false, false>;
+  if (a.eps_in) k = a.importance ? mlp_rollout_kernel<Dyn, Cost, true, true> : mlp_rollout_kernel<Dyn, Cost, true, false>;
+  else if (a.importance) k = mlp_rollout_kernel<Dyn, Cost, false, true>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k<<<grid, block, smem, st>>>(a, dyn, cost);
+  return cudaGetLastError();
+}
+
+template <class Dyn>
+cudaError_t rollout(const Dyn& dyn, const IterArgs& a, int cost_kind, cudaStream_t st) {
+  switch (cost_kind) {
+    case 0: return launch(a, dyn, make_road(a.cost), st);
+    case 3: return launch(a, dyn, make_quad<7>(a.cost), st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace mlpk
+
+namespace {
+template <bool F>
+MlpDyn<F> mlp_make(const DynParams& p) {
+  MlpDyn<F> d;
+  d.w = p.tensor;
+  return d;
+}
+template <bool F>
+cudaError_t mlp_rollout(const IterArgs& a, int ck, cudaStream_t st) {
+  return mlpk::rollout(mlp_make<F>(a.dyn), a, ck, st);
+}
+template <bool F>
+cudaError_t mlp_update(const IterArgs& a, cudaStream_t st) {
+  return launch_update_t(a, mlp_make<F>(a.dyn), st);
+}
+template <bool F>
+cudaError_t mlp_combine(const IterArgs& a, cudaStream_t st) {
+  return launch_combine_t(a, mlp_make<F>(a.dyn), st);
+}
+cudaError_t mlp_generate(const IterArgs& a, float* e, uint8_t* f, cudaStream_t st) {
+  return launch_generate_t<2>(a, e, f, st);
+}
+}  // namespace
+
+ModelOps ops_mlp(bool fma_libm) {
+  if (fma_libm) return ModelOps{mlp_rollout<true>, launch_weights, mlp_update<true>, mlp_combine<true>, mlp_generate, 7, 2, 7};
+  return ModelOps{mlp_rollout<false>, launch_weights, mlp_update<false>, mlp_combine<false>, mlp_generate, 7, 2, 7};
+}
+
+}  // namespace smpc_dev

@@ -225,6 +225,14 @@ void validate(smpc_ctx* c) {
         throw RuntimeError{"quadrotor: thrust_max must exceed hover thrust and rate_max must be > 0"};
       c->ops = ops_quadrotor();
       break;
+    case SMPC_DYN_MLP:  // builder-defined (models.cuh:MlpDyn, tcgen05 rollout in mlp.cu)
+      if (!p.dyn_tensor || p.dyn_tensor_len != mlp_layout::TOTAL)
+        throw RuntimeError{"mlp: dyn_tensor must hold " + std::to_string(mlp_layout::TOTAL) +
+                           " floats (W1 b1 W2 b2 W3 b3, smpc_b200.h)"};
+      for (int64_t k = 0; k < p.dyn_tensor_len; ++k)
+        if (!std::isfinite(p.dyn_tensor[k])) throw RuntimeError{"mlp: network parameters must be finite"};
+      c->ops = ops_mlp(c->fma);
+      break;
     default: throw ConfigError{"dynamics.kind is not recognized"};
   }
   c->nx = c->ops.nx, c->nu = c->ops.nu, c->ny = c->ops.ny;
@@ -679,6 +687,9 @@ smpc_status smpc_create(const smpc_problem* problem, smpc_ctx** out) {
     if (p.std_per_step) c->std_per_step.assign(p.std_per_step, p.std_per_step + TU);
     if (p.n_step_sizes > 0) c->step_sizes.assign(p.step_sizes, p.step_sizes + p.n_step_sizes);
     if (p.costmap) c->costmap.assign(p.costmap, p.costmap + (size_t)p.costmap_cells_x * p.costmap_cells_y);
+    std::vector<float> dyn_tensor;
+    if (p.dyn_tensor) dyn_tensor.assign(p.dyn_tensor, p.dyn_tensor + p.dyn_tensor_len);
+    p.dyn_tensor = nullptr;
     p.std_per_step = nullptr;
     p.step_sizes = nullptr;
     p.costmap = nullptr;
@@ -750,6 +761,10 @@ smpc_status smpc_create(const smpc_problem* problem, smpc_ctx** out) {
       const size_t cells = (size_t)p.costmap_cells_x * p.costmap_cells_y;
       c->d_costmap = dalloc<uint8_t>(cells);
       if (!c->costmap.empty()) CK(cudaMemcpy(c->d_costmap, c->costmap.data(), cells, cudaMemcpyHostToDevice));
+    }
+    if (!dyn_tensor.empty()) {
+      c->d_dyn_tensor = dalloc<float>(dyn_tensor.size());
+      CK(cudaMemcpy(c->d_dyn_tensor, dyn_tensor.data(), sizeof(float) * dyn_tensor.size(), cudaMemcpyHostToDevice));
     }
     const uint32_t n_tab = tail_table_size(nullptr, nullptr);
     c->d_tail = dalloc<float>(2 * (size_t)n_tab);

@@ -200,6 +200,8 @@ class Scenario:
     target: Optional[Sequence[float]] = None
     weights: Optional[Sequence[float]] = None
     costmap: Optional[Costmap] = None
+    # SMPC_DYN_MLP parameter blob (1412 floats, see autorally_mlp_weights)
+    mlp_weights: Optional[np.ndarray] = None
     # controller (scenario.hpp:83-94)
     controller: str = "mppi"
     step_size: float = 1.0
@@ -298,6 +300,12 @@ class Scenario:
         p.nominal_reset_bound = float(self.nominal_reset_bound)
         p.elite_fraction = float(self.elite_fraction)
         p.dynamics_kind = DYNAMICS_KINDS[self.dynamics]
+        if self.dynamics == "mlp":
+            wb = np.ascontiguousarray(self.mlp_weights if self.mlp_weights is not None else autorally_mlp_weights(),
+                                      np.float32).ravel()
+            keep.append(wb)
+            p.dyn_tensor = wb.ctypes.data_as(ctypes.POINTER(ctypes.c_float))
+            p.dyn_tensor_len = wb.size
         dp = self._dyn_params()
         p.n_dyn_params = len(dp)
         for i, v in enumerate(dp):
@@ -386,6 +394,39 @@ def quadrotor_scenario(num_samples: int = 8192, horizon: int = 100, seed: int = 
     return Scenario(num_samples=num_samples, horizon=horizon, dt=0.02, lambda_=1.0,
                     control_std=(0.5, 0.5, 0.5, 2.0), rng_seed=seed, dynamics="quadrotor", cost="quadratic",
                     target=target, weights=weights, initial_state={"QW": 1.0})
+
+
+MLP_LAYOUT = dict(W1=(32, 6), b1=(32,), W2=(32, 32), b2=(32,), W3=(4, 32), b3=(4,))
+
+
+def autorally_mlp_weights(seed: int = 0) -> np.ndarray:
+    """Random-init AutoRally-style dynamics network 6-32-32-4 (tanh), flattened
+    in the SMPC_DYN_MLP blob order W1 b1 W2 b2 W3 b3 (1412 floats). Synthetic
+    (no checkpoint is available offline): fan-in scaled Gaussian weights, the
+    output layer scaled so accelerations stay O(1) over a 2 s horizon."""
+    rng = np.random.default_rng(seed)
+    parts = []
+    for name, shape in MLP_LAYOUT.items():
+        fan_in = shape[1] if len(shape) == 2 else 1
+        if name.startswith("W"):
+            scale = (0.5 if name == "W3" else 1.0) / math.sqrt(fan_in)
+            parts.append(rng.standard_normal(shape) * scale)
+        else:
+            parts.append(rng.standard_normal(shape) * 0.1)
+    return np.concatenate([q.ravel() for q in parts]).astype(np.float32)
+
+
+def autorally_scenario(num_samples: int = 8192, horizon: int = 100, seed: int = 21, controller: str = "mppi",
+                       weights_seed: int = 0) -> Scenario:
+    """C4: AutoRally-style neural dynamics (tcgen05 rollout), quadratic cost on
+    lateral offset / heading / a 4 m/s forward-speed target (BASELINE.json
+    configs[3]; builder-defined model). controller="tube" gives the dual
+    nominal/real rollout."""
+    return Scenario(num_samples=num_samples, horizon=horizon, dt=0.02, lambda_=1.0, control_std=(0.3, 0.3),
+                    rng_seed=seed, dynamics="mlp", cost="quadratic",
+                    target=[0.0, 0.0, 0.0, 0.0, 4.0, 0.0, 0.0], weights=[0.0, 0.5, 1.0, 0.1, 1.0, 0.1, 0.1],
+                    mlp_weights=autorally_mlp_weights(weights_seed), controller=controller,
+                    initial_state={"V_X": 2.0})
 
 
 def synthetic_costmap(seed: int = 3) -> Costmap:

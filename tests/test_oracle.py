@@ -220,3 +220,14 @@ def test_quadrotor_hover_is_an_equilibrium(port):
     # thrust is clamped to [0, T_max]
     xc, _ = port.step(sc, x, np.array([0, 0, 0, 1e6], np.float32), np.float32(0.02))
     assert abs(xc[5] - 0.02 * (39.24 - 9.81)) < 1e-5
+
+
+def test_mlp_oracle_zero_network_is_pure_kinematics(port):
+    """With an all-zero network the MLP model is the AutoRally kinematics only."""
+    sc = S.autorally_scenario(num_samples=4, horizon=5)
+    sc.mlp_weights = np.zeros(1412, np.float32)
+    x = np.array([0, 0, 0.5, 0, 2.0, 0.5, 0.3], np.float32)
+    xn, _ = port.step(sc, x, np.array([0.2, 0.4], np.float32), np.float32(0.1))
+    c, s = np.cos(np.float32(0.5)), np.sin(np.float32(0.5))
+    assert abs(xn[0] - 0.1 * (2.0 * c - 0.5 * s)) < 1e-6 and abs(xn[1] - 0.1 * (2.0 * s + 0.5 * c)) < 1e-6
+    assert abs(xn[2] - 0.53) < 1e-6 and np.array_equal(xn[3:], x[3:])
