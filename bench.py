@@ -11,7 +11,8 @@ samples, T = 100 (the large-sample sweep config the metric is quoted on for
 with the WorkerPool chunk rule).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--workload di|cartpole|diffdrive|quadrotor] [--samples N] [--scaling strong|weak]
+                  [--workload di|cartpole|diffdrive|quadrotor|autorally] [--samples N]
+                  [--scaling strong|weak]
 
 Rank 0 prints ONE JSON line. `value` = samples/s of the whole job from
 device-resident graph replays (CUDA events on the context stream, L2 flushed
@@ -40,8 +41,12 @@ from paper_2409_07563_b200 import scenario as S  # noqa: E402
 # quadrotor (builder-defined): noise 4x29, control 4, clamp 8,
 # derivative 49, Euler 26, quaternion normalisation 11 (+1 sqrt); FP64:
 # quadratic cost 13x4 + total 1 + importance 4x3.
-FP32_OPS_PER_SAMPLE_STEP = {"di": 83, "cartpole": 56, "diffdrive": 90, "quadrotor": 214}
-FP64_OPS_PER_SAMPLE_STEP = {"di": 9, "cartpole": 23, "diffdrive": 19, "quadrotor": 65}
+# autorally (C4, Tube S=2; per system-sample-step): SIMT layers 1 and 3 =
+# (6x32 + 32x4) MACs = 640 FP32 ops + 64 tanh, noise 2x29, kinematics 6,
+# Euler 14; tensor layer 2 = 32x32 MACs = 2048 flops (3xTF32 issues 3x that).
+FP32_OPS_PER_SAMPLE_STEP = {"di": 83, "cartpole": 56, "diffdrive": 90, "quadrotor": 214, "autorally": 718}
+FP64_OPS_PER_SAMPLE_STEP = {"di": 9, "cartpole": 23, "diffdrive": 19, "quadrotor": 65, "autorally": 41}
+TENSOR_FLOPS_PER_SAMPLE_STEP = {"autorally": 2048}
 # workloads whose model exists in the reference (oracle/_ref can time them)
 REFERENCE_WORKLOADS = ("di", "cartpole", "diffdrive")
 
@@ -55,6 +60,8 @@ def make_scenario(workload: str, n: int) -> S.Scenario:
         return S.diff_drive_nav_scenario(num_samples=n, horizon=56, seed=42)
     if workload == "quadrotor":
         return S.quadrotor_scenario(num_samples=n, horizon=100, seed=13)
+    if workload == "autorally":
+        return S.autorally_scenario(num_samples=n, horizon=100, seed=21, controller="tube")
     raise SystemExit(f"unknown workload {workload}")
 
 
@@ -62,7 +69,8 @@ def workload_name(workload: str, n: int) -> str:
     return {"di": f"C5 double_integrator+circle_track MPPI N={n} T=100",
             "cartpole": f"C1 cartpole+quadratic MPPI N={n} T=100",
             "diffdrive": f"C3 diff_drive+diff_drive_nav(costmap 110x110) MPPI N={n} T=56",
-            "quadrotor": f"C2 quadrotor(13-state)+quadratic tracking MPPI N={n} T=100"}[workload]
+            "quadrotor": f"C2 quadrotor(13-state)+quadratic tracking MPPI N={n} T=100",
+            "autorally": f"C4 AutoRally MLP dynamics (tcgen05) Tube-MPPI N={n} T=100"}[workload]
 
 
 class ClockSampler:
@@ -274,7 +282,8 @@ def run_ours(args):
         ctl.synchronize()
     roll_ms_total, roll_n = ctl.rollout_timing(False)
     roll_ms = roll_ms_total / max(roll_n, 1)
-    ops_per_launch = (shard[1] - shard[0]) * sc.horizon * FP32_OPS_PER_SAMPLE_STEP[args.workload]
+    systems = 2 if sc.controller == "tube" else 1
+    ops_per_launch = (shard[1] - shard[0]) * sc.horizon * systems * FP32_OPS_PER_SAMPLE_STEP[args.workload]
     peak = ctypes.c_double()
     _lib.load().smpc_measure_fp32_peak(device, ctypes.byref(peak))
     achieved = ops_per_launch / (roll_ms * 1e-3) / 1e12
@@ -288,6 +297,21 @@ def run_ours(args):
                                f"{FP64_OPS_PER_SAMPLE_STEP[args.workload]} FP64 ops per sample-step "
                                f"x {shard[1] - shard[0]} samples x {sc.horizon} steps per launch",
                 "hbm_peak_gbs_measured": None}
+    if args.workload in TENSOR_FLOPS_PER_SAMPLE_STEP:
+        # tcgen05 layer: algorithmic TF32 flops / rollout time vs the dense TF32 peak
+        # (half the measured bf16 peak in MEASURED_PEAKS.json; B200_PROFILING.md fallback 1125 TF/s)
+        tf = (shard[1] - shard[0]) * sc.horizon * systems * TENSOR_FLOPS_PER_SAMPLE_STEP[args.workload]
+        bf16 = None
+        try:
+            with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+                bf16 = json.load(f).get("bf16_tflops")
+        except (OSError, ValueError):
+            pass
+        tpeak = bf16 / 2 if bf16 else 1125.0
+        roofline["tensor"] = {"achieved": tf / (roll_ms * 1e-3) / 1e12, "peak": tpeak, "unit": "TFLOP/s (tf32)",
+                              "frac": tf / (roll_ms * 1e-3) / 1e12 / tpeak,
+                              "algorithmic": f"{TENSOR_FLOPS_PER_SAMPLE_STEP[args.workload]} flops per sample-step "
+                                             "(32x32 layer; 3xTF32 issues 3 MMAs per product)"}
 
     # ---- e2e: public C-ABI call with host buffers (H2D x0, D2H solution) -----
     barrier(dist, local)
@@ -298,7 +322,7 @@ def run_ours(args):
     e2e_s = max_over_ranks(dist, time.perf_counter() - t0)
     e2e_ms = e2e_s * 1e3 / e2e_steps
     n_x, n_u, n_y = sc.dims
-    d2h = 4 * (sc.horizon * n_u + (sc.horizon + 1) * n_x + sc.horizon * n_y) + 128
+    d2h = systems * 4 * (sc.horizon * n_u + (sc.horizon + 1) * n_x + sc.horizon * n_y) + 128
     e2e = {"value": n_global * 1000.0 / e2e_ms, "unit": "samples/s", "ms_per_step": e2e_ms,
            "h2d_bytes_per_step": 4 * n_x, "d2h_bytes_per_step": d2h,
            "api": "smpc_compute_control (MppiController::compute_control)"}
@@ -339,7 +363,7 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="di", choices=["di", "cartpole", "diffdrive", "quadrotor"])
+    ap.add_argument("--workload", default="di", choices=["di", "cartpole", "diffdrive", "quadrotor", "autorally"])
     ap.add_argument("--samples", type=int, default=1 << 20)
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
     ap.add_argument("--roofline-steps", type=int, default=20)

@@ -64,6 +64,38 @@ __device__ __forceinline__ float to_tf32(float x) {
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
+// ---- packed f32x2 helpers (the MLP path has no bit-exactness contract, so
+// FFMA2 contraction is used freely here) ----------------------------------
+typedef unsigned long long f2;
+__device__ __forceinline__ f2 pk(float lo, float hi) { return f2pack(lo, hi); }
+__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) { return f2fma(a, b, c); }
+__device__ __forceinline__ float ex2f(float x) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float rcpf(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+// Two tanh at once: sign(x) (1 - 2 / (2^{2|x| log2 e} + 1)); abs error ~1e-7.
+__device__ __forceinline__ f2 tanh2(f2 x) {
+  float a, b;
+  f2unpack(x, a, b);
+  const f2 ax = pk(fabsf(a), fabsf(b));
+  const f2 t = fma2(ax, f2splat_bits(0x4038AA3Bu) /* 2 log2 e */, 0ull);
+  float t0, t1;
+  f2unpack(t, t0, t1);
+  const f2 den = fma2(pk(ex2f(t0), ex2f(t1)), f2splat_bits(0x3F800000u), f2splat_bits(0x3F800000u));  // e + 1
+  float d0, d1;
+  f2unpack(den, d0, d1);
+  const f2 r = fma2(pk(rcpf(d0), rcpf(d1)), f2splat_bits(0xC0000000u) /* -2 */, f2splat_bits(0x3F800000u));
+  float r0, r1;
+  f2unpack(r, r0, r1);
+  return pk(copysignf(r0, a), copysignf(r1, b));
+}
+
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
@@ -124,7 +156,7 @@ __global__ void __launch_bounds__(kTile, 4) mlp_rollout_kernel(const IterArgs a,
   if (aborted(a)) return;
   const int T = a.T, TU = T * NU;
   const Smem L(S, TU);
-  float* prm = reinterpret_cast<float*>(smem + L.params);  // W1 [0,192) b1 [192,224) b2 [224,256) W3 [256,384) b3 [384,388)
+  float* prm = reinterpret_cast<float*>(smem + L.params);  // W1T [0,192) b1 [192,224) b2 [224,256) W3T [256,384) b3 [384,388)
   const float* sW1 = prm;
   const float* sB1 = prm + HID * IN;
   const float* sB2 = sB1 + HID;
@@ -146,9 +178,11 @@ __global__ void __launch_bounds__(kTile, 4) mlp_rollout_kernel(const IterArgs a,
     *reinterpret_cast<float*>(smem + L.w2hi + core_off(n, k)) = hi;
     *reinterpret_cast<float*>(smem + L.w2lo + core_off(n, k)) = to_tf32(v - hi);
   }
-  for (int e = tid; e < HID * IN + HID; e += kTile) prm[e] = __ldg(w + W1 + e);         // W1, b1
-  for (int e = tid; e < HID; e += kTile) prm[HID * IN + HID + e] = __ldg(w + B2 + e);  // b2
-  for (int e = tid; e < OUT * HID + OUT; e += kTile) prm[HID * IN + 2 * HID + e] = __ldg(w + W3 + e);  // W3, b3
+  // SIMT layers, transposed for packed broadcast reads: W1T[k][j], b1, b2, W3T[j][q], b3
+  for (int e = tid; e < HID * IN; e += kTile) prm[(e % IN) * HID + e / IN] = __ldg(w + W1 + e);
+  for (int e = tid; e < HID; e += kTile) prm[HID * IN + e] = __ldg(w + B1 + e), prm[HID * IN + HID + e] = __ldg(w + B2 + e);
+  for (int e = tid; e < OUT * HID; e += kTile) prm[HID * IN + 2 * HID + (e % HID) * OUT + e / HID] = __ldg(w + W3 + e);
+  for (int e = tid; e < OUT; e += kTile) prm[HID * IN + 2 * HID + OUT * HID + e] = __ldg(w + B3 + e);
   for (int k = tid; k < TU; k += kTile) {
     sigma_s[k] = a.sigma[k];
     if (IMP) sig2_s[k] = a.sig2[k];
@@ -206,18 +240,28 @@ __global__ void __launch_bounds__(kTile, 4) mlp_rollout_kernel(const IterArgs a,
     dyn.clamp_control(u, uc);
     // ---- layer 1 (SIMT) -> this sample's row of the hi/lo A operand
     const float in[IN] = {x[3], x[4], x[5], x[6], uc[0], uc[1]};
+    f2 inb[IN];
+#pragma unroll
+    for (int k = 0; k < IN; ++k) inb[k] = pk(in[k], in[k]);
 #pragma unroll
     for (int j0 = 0; j0 < HID; j0 += 4) {
+      // units j0..j0+3 as two packed pairs, 6 FFMA2 each
+      const ulonglong2 bb = *reinterpret_cast<const ulonglong2*>(sB1 + j0);
+      f2 acc0 = bb.x, acc1 = bb.y;
+#pragma unroll
+      for (int k = 0; k < IN; ++k) {
+        const ulonglong2 wk = *reinterpret_cast<const ulonglong2*>(sW1 + k * HID + j0);
+        acc0 = fma2(wk.x, inb[k], acc0);
+        acc1 = fma2(wk.y, inb[k], acc1);
+      }
+      float h[4];
+      f2unpack(tanh2(acc0), h[0], h[1]);
+      f2unpack(tanh2(acc1), h[2], h[3]);
       float hv[4], lv[4];
 #pragma unroll
       for (int jj = 0; jj < 4; ++jj) {
-        const int j = j0 + jj;
-        float acc = sB1[j];
-#pragma unroll
-        for (int k = 0; k < IN; ++k) acc += sW1[j * IN + k] * in[k];
-        const float h = mlp_tanh(acc);
-        hv[jj] = to_tf32(h);
-        lv[jj] = to_tf32(h - hv[jj]);
+        hv[jj] = to_tf32(h[jj]);
+        lv[jj] = to_tf32(h[jj] - hv[jj]);
       }
       *reinterpret_cast<float4*>(hhi + core_off(tid, j0)) = make_float4(hv[0], hv[1], hv[2], hv[3]);
       *reinterpret_cast<float4*>(hlo + core_off(tid, j0)) = make_float4(lv[0], lv[1], lv[2], lv[3]);
@@ -247,15 +291,24 @@ __global__ void __launch_bounds__(kTile, 4) mlp_rollout_kernel(const IterArgs a,
     // ---- epilogue: layer 3 + kinematics + Euler + running cost
     float d2[HID];
     tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16), d2);
-    float o[OUT];
+    const ulonglong2 b3v = *reinterpret_cast<const ulonglong2*>(sB3);
+    f2 o01 = b3v.x, o23 = b3v.y;
 #pragma unroll
-    for (int q = 0; q < OUT; ++q) o[q] = sB3[q];
-#pragma unroll
-    for (int j = 0; j < HID; ++j) {
-      const float h2 = mlp_tanh(d2[j] + sB2[j]);
-#pragma unroll
-      for (int q = 0; q < OUT; ++q) o[q] += sW3[q * HID + j] * h2;
+    for (int j = 0; j < HID; j += 2) {
+      const f2 hb = fma2(pk(d2[j], d2[j + 1]), f2splat_bits(0x3F800000u), *reinterpret_cast<const f2*>(sB2 + j));
+      float h0, h1;
+      f2unpack(tanh2(hb), h0, h1);
+      const ulonglong2 w0 = *reinterpret_cast<const ulonglong2*>(sW3 + j * OUT);        // W3T[j][0..3]
+      const ulonglong2 w1 = *reinterpret_cast<const ulonglong2*>(sW3 + (j + 1) * OUT);  // W3T[j+1][0..3]
+      const f2 hh0 = pk(h0, h0), hh1 = pk(h1, h1);
+      o01 = fma2(w0.x, hh0, o01);
+      o23 = fma2(w0.y, hh0, o23);
+      o01 = fma2(w1.x, hh1, o01);
+      o23 = fma2(w1.y, hh1, o23);
     }
+    float o[OUT];
+    f2unpack(o01, o[0], o[1]);
+    f2unpack(o23, o[2], o[3]);
     float dx[NX];
     dyn.kinematics(x, dx);
 #pragma unroll

@@ -762,6 +762,11 @@ smpc_status smpc_create(const smpc_problem* problem, smpc_ctx** out) {
       c->d_costmap = dalloc<uint8_t>(cells);
       if (!c->costmap.empty()) CK(cudaMemcpy(c->d_costmap, c->costmap.data(), cells, cudaMemcpyHostToDevice));
     }
+    if (p.dynamics_kind == SMPC_DYN_MLP) {  // + W2 transposed for the warp-cooperative nominal rollout
+      using namespace mlp_layout;
+      for (int k = 0; k < HID; ++k)
+        for (int j = 0; j < HID; ++j) dyn_tensor.push_back(dyn_tensor[W2 + j * HID + k]);
+    }
     if (!dyn_tensor.empty()) {
       c->d_dyn_tensor = dalloc<float>(dyn_tensor.size());
       CK(cudaMemcpy(c->d_dyn_tensor, dyn_tensor.data(), sizeof(float) * dyn_tensor.size(), cudaMemcpyHostToDevice));
