@@ -81,6 +81,10 @@ class Oracle:
                                                  ctypes.POINTER(SmpcWeightSummary), ctypes.POINTER(_OracleErr)]
             L.oracle_partial_sort.argtypes = [_f64p, ctypes.c_int64, ctypes.c_int64,
                                               np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS")]
+            L.oracle_clamp_control.argtypes = [ctypes.POINTER(SmpcProblem), _f32p, _f32p]
+            L.oracle_wrap_angle.argtypes = [ctypes.c_float]
+            L.oracle_wrap_angle.restype = ctypes.c_float
+            L.oracle_angular_channel.argtypes = [ctypes.POINTER(SmpcProblem)]
             L.oracle_running_cost.argtypes = [ctypes.POINTER(SmpcProblem), _f32p]
             L.oracle_running_cost.restype = ctypes.c_double
             L.oracle_terminal_cost.argtypes = [ctypes.POINTER(SmpcProblem), _f32p]
@@ -108,6 +112,10 @@ class Oracle:
             L.ref_get_mean.argtypes = [ctypes.c_void_p, _f32p]
             L.ref_shift_control_sequence.argtypes = [ctypes.c_void_p, ctypes.c_double, ctypes.c_double, *E]
             L.ref_compute_control.argtypes = [ctypes.c_void_p, _f32p, _f32p, _f32p, _f32p, ctypes.c_void_p, _f64p, *E]
+            L.ref_run_control_loop.argtypes = [ctypes.POINTER(SmpcProblem), ctypes.c_double, ctypes.c_double,
+                                               ctypes.c_double, _f32p, ctypes.c_double, ctypes.c_int,
+                                               ctypes.POINTER(ctypes.c_double), ctypes.c_void_p,
+                                               ctypes.POINTER(ctypes.c_int64), *E]
             L.ref_tube_compute_control.argtypes = [ctypes.c_void_p, _f32p, _f32p, _f32p, _f64p, _f32p, _f32p, _f64p,
                                                    _f32p, *E]
 
@@ -349,3 +357,85 @@ class OracleController:
         return dict(nominal_controls=nc.reshape(T, n_u), nominal_states=ns.reshape(T + 1, n_x),
                     real_controls=rcn.reshape(T, n_u), real_states=rs.reshape(T + 1, n_x),
                     nominal_state=nominal_state_used, nominal=sn, real=sr)
+
+
+def shift_mean(mean: np.ndarray, T: int, n_u: int, dt: float, elapsed_s: float, dt_min: float) -> np.ndarray:
+    """Controller::shift_control_sequence (controllers.cpp:68-84) on a flat mean."""
+    if elapsed_s <= 0.0:
+        return mean
+    quantized = float(np.rint(elapsed_s / dt_min)) * dt_min
+    steps = int(np.rint(quantized / dt))
+    if steps <= 0:
+        return mean
+    m = mean.reshape(T, n_u)
+    if steps >= T:
+        return np.zeros_like(mean)
+    out = np.concatenate([m[steps:], np.repeat(m[T - 1:T], steps, axis=0)])
+    return np.ascontiguousarray(out.ravel(), np.float32)
+
+
+def control_loop(sc: Scenario, duration_s: float, kind: str = "port", workers: int = 1):
+    """Plant::run_control_loop (plant.cpp:133-181) with SimulatedSystem::step
+    (plant.cpp:31-48) on a checker controller, in Python around the C oracle
+    (kind "port") or the reference controller (kind "reference"). Returns
+    (accumulated_cost, rows[steps, 2 + n_x + n_u] = {t, x, u_applied, c})."""
+    port = Oracle("port")
+    ctl = OracleController(sc, kind, workers=workers)
+    n_x, n_u, n_y = sc.dims
+    T, dt = sc.horizon, sc.dt
+    p = sc.to_problem()
+    steps = int(round(duration_s / dt))
+    interval = 1.0 / sc.replan_rate
+    sim_seed = (int(sc.rng_seed) ^ 0x9E3779B97F4A7C15) & 0xFFFFFFFFFFFFFFFF
+    scale = np.float32(sc.disturbance_std * np.sqrt(dt))
+    ang = port.lib.oracle_angular_channel(ctypes.byref(p))
+    x = np.ascontiguousarray(sc.x0(), np.float32)
+    next_replan_t, solution_t, solved_once = 0.0, 0.0, False
+    sol = None
+    rows = np.zeros((steps, 2 + n_x + n_u))
+    acc = 0.0
+    for step in range(steps):
+        t = step * dt
+        if not solved_once or t >= next_replan_t - 1e-9:
+            if solved_once:
+                if kind == "reference":
+                    buf = ctypes.create_string_buffer(512)
+                    ctl.o.lib.ref_shift_control_sequence(ctl.handle, t - solution_t, sc.dt_min, buf, 512)
+                else:
+                    ctl.set_mean(shift_mean(ctl.mean, T, n_u, dt, t - solution_t, sc.dt_min))
+            sol = ctl.compute_control(x)
+            solution_t, solved_once = t, True
+            while next_replan_t <= t + 1e-9:
+                next_replan_t += interval
+        idx = min(max(int(np.floor((t - solution_t) / dt)), 0), T - 1)
+        u = np.ascontiguousarray(sol["controls"][idx], np.float32)
+        uc = np.zeros(n_u, np.float32)
+        port.lib.oracle_clamp_control(ctypes.byref(p), u, uc)
+        c = port.running_cost(sc, x)
+        rows[step] = np.concatenate([[t], x, uc, [c]])
+        acc += c
+        xn, _ = port.step(sc, x, uc, np.float32(dt))
+        if scale > 0:
+            for ch in range(n_x):
+                z = port.quad(sim_seed, step & 0xFFFFFFFF, ch // 4, 0)[ch % 4]
+                xn[ch] = np.float32(xn[ch] + np.float32(scale * z))
+            if ang >= 0:
+                xn[ang] = port.lib.oracle_wrap_angle(float(xn[ang]))
+        x = xn
+    return acc, rows
+
+
+def reference_control_loop(sc: Scenario, duration_s: float, workers: int = 1):
+    """The reference's own Plant::run_control_loop (oracle/_ref). Same return as control_loop."""
+    o = Oracle("reference")
+    n_x, n_u, _ = sc.dims
+    steps = int(round(duration_s / sc.dt))
+    rows = np.zeros((steps, 2 + n_x + n_u))
+    acc, n = ctypes.c_double(), ctypes.c_int64()
+    buf = ctypes.create_string_buffer(512)
+    p = sc.to_problem()
+    rc = o.lib.ref_run_control_loop(ctypes.byref(p), sc.replan_rate, sc.dt_min, sc.disturbance_std,
+                                    np.ascontiguousarray(sc.x0(), np.float32), duration_s, workers, ctypes.byref(acc),
+                                    rows.ctypes.data, ctypes.byref(n), buf, 512)
+    Oracle._check(rc, buf.value)
+    return acc.value, rows[:n.value]

@@ -61,8 +61,16 @@ def fixture_scenarios():
     return sc
 
 
+def closed_loop_scenarios():
+    sweep = S.default_sweep_scenario()  # bench.cpp:186-202
+    sweep.num_samples, sweep.step_size, sweep.rng_seed, sweep.disturbance_std = 256, 0.6, 3, 0.3
+    nav = S.diff_drive_nav_scenario(num_samples=200, horizon=20, seed=8)
+    nav.replan_rate, nav.disturbance_std = 20.0, 0.2  # replans every 2.5 steps: shifts + idx > 0
+    return {"loop_sweep_dmd": (sweep, 200), "loop_nav_replan20": (nav, 100)}
+
+
 def scenario_record(sc: S.Scenario) -> dict:
-    d = {k: v for k, v in vars(sc).items() if k != "costmap"}
+    d = {k: v for k, v in vars(sc).items() if k not in ("costmap", "mlp_weights")}
     d["control_std"] = list(sc.control_std)
     return d
 
@@ -121,6 +129,14 @@ def main():
         np.savez_compressed(os.path.join(OUT, f"{name}.npz"), **rec)
         index[name] = scenario_record(sc)
         print(name, "rho", rho, "argmin", am, "bytes", os.path.getsize(os.path.join(OUT, f"{name}.npz")))
+    # Closed loops: the reference's own Plant::run_control_loop (plant.cpp:133-181).
+    from oracle.bindings import reference_control_loop
+    for name, (sc, steps) in closed_loop_scenarios().items():
+        acc, rows = reference_control_loop(sc, steps * sc.dt)
+        np.savez_compressed(os.path.join(OUT, f"{name}.npz"), accumulated_cost=np.float64(acc), rows=rows,
+                            steps=np.int64(steps))
+        index[name] = scenario_record(sc)
+        print(name, "accumulated cost", acc)
     # Random123 Philox4x32-10 known-answer vectors and reference normals.
     kat = {
         "philox": [

@@ -22,6 +22,7 @@
 #include "smpc/costs.hpp"
 #include "smpc/dynamics.hpp"
 #include "smpc/engine.hpp"
+#include "smpc/plant.hpp"
 #include "smpc/rng.hpp"
 #include "smpc/sampling.hpp"
 
@@ -337,6 +338,42 @@ void* ref_controller_create(const smpc_problem* p, int workers, int strategy, ch
 }
 
 void ref_controller_destroy(void* h) { delete static_cast<RefController*>(h); }
+
+// Plant::run_control_loop (plant.cpp:133-181) on a fresh single-system
+// controller with the reference's own Plant and SimulatedSystem (seeded as
+// make_simulated_system does, plant.cpp:224-230). rows: steps x (2+n_x+n_u).
+int ref_run_control_loop(const smpc_problem* p, double replan_rate, double dt_min, double disturbance_std,
+                         const float* x0, double duration_s, int workers, double* accumulated, double* rows,
+                         int64_t* n_rows, char* err, size_t errn) {
+  try {
+    void* h = ref_controller_create(p, workers, 1, err, errn);
+    if (!h) return 3;
+    std::unique_ptr<RefController> rc(static_cast<RefController*>(h));
+    std::shared_ptr<Controller> ctl(std::move(rc->ctl));
+    PlantConfig pc;
+    pc.replan_rate = replan_rate;
+    pc.dt_min = dt_min;
+    Plant plant(pc, ctl);
+    auto dyn = make_dyn(p);
+    SimulatedSystem sim(dyn, state(x0, dyn->dims().n_x), disturbance_std, p->seed ^ 0x9E3779B97F4A7C15ull);
+    const LoopResult r = plant.run_control_loop(sim, duration_s);
+    *accumulated = r.accumulated_cost;
+    *n_rows = (int64_t)r.rows.size();
+    if (rows) {
+      size_t k = 0;
+      for (const auto& row : r.rows) {
+        rows[k++] = row.t;
+        for (int i = 0; i < row.x.dim(); ++i) rows[k++] = row.x[i];
+        for (int i = 0; i < row.u.dim(); ++i) rows[k++] = row.u[i];
+        rows[k++] = row.running_cost;
+      }
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    set_err(err, errn, e.what());
+    return 3;
+  }
+}
 
 int ref_set_mean(void* h, const float* mean) {
   auto* rc = static_cast<RefController*>(h);

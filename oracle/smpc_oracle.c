@@ -793,6 +793,15 @@ int oracle_tube_compute_control(const smpc_problem* p, float* nominal_mean, floa
   return 0;
 }
 
+/* DynamicsModel::clamp_control (dynamics.cpp:31-39) and wrap_angle (types.hpp:36-42) for the closed-loop checker. */
+void oracle_clamp_control(const smpc_problem* p, const float* u, float* out) {
+  oracle_dims d;
+  if (oracle_dims_of(p, &d, NULL)) return;
+  clamp_control(p, u, out, d.n_u);
+}
+float oracle_wrap_angle(float a) { return wrap_angle(a); }
+int oracle_angular_channel(const smpc_problem* p) { return angular_channel(p); }
+
 /* CostFunction::running_cost_raw / terminal_cost_raw (costs.hpp:24-25) for unit tests. */
 double oracle_running_cost(const smpc_problem* p, const float* y) { return running_cost(p, y); }
 double oracle_terminal_cost(const smpc_problem* p, const float* y) { return terminal_cost(p, y); }

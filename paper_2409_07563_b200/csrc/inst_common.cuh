@@ -70,11 +70,33 @@ cudaError_t rollout_dispatch(const Dyn& dyn, const IterArgs& a, int cost_kind, c
   return cudaErrorInvalidValue;
 }
 
+template <class Dyn>
+cudaError_t plant_dispatch(const Dyn& dyn, const IterArgs& a, int cost_kind, const PlantStepArgs& p,
+                           cudaStream_t st) {
+  switch (cost_kind) {
+    case 0:
+      if constexpr (Dyn::NY >= 2) return launch_plant_step_t(a, dyn, make_road(a.cost), p, st);
+      break;
+    case 1:
+      if constexpr (Dyn::NY == 4 && Dyn::NU == 2) return launch_plant_step_t(a, dyn, make_circle(a.cost), p, st);
+      break;
+    case 2:
+      if constexpr (Dyn::NY == 3 && Dyn::NU == 2) return launch_plant_step_t(a, dyn, make_nav(a.cost), p, st);
+      break;
+    case 3:
+      return launch_plant_step_t(a, dyn, make_quad<Dyn::NY>(a.cost), p, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
 #define SMPC_DEFINE_OPS(NAME, DYN_T, ...)                                                       \
   namespace {                                                                                   \
   DYN_T NAME##_make(const DynParams& p) { __VA_ARGS__ }                                         \
   cudaError_t NAME##_rollout(const IterArgs& a, int ck, cudaStream_t st) {                       \
     return rollout_dispatch(NAME##_make(a.dyn), a, ck, st);                                      \
+  }                                                                                             \
+  cudaError_t NAME##_plant(const IterArgs& a, int ck, const PlantStepArgs& p, cudaStream_t st) {   \
+    return plant_dispatch(NAME##_make(a.dyn), a, ck, p, st);                                     \
   }                                                                                             \
   cudaError_t NAME##_update(const IterArgs& a, cudaStream_t st) {                                \
     return launch_update_t(a, NAME##_make(a.dyn), st);                                           \
@@ -86,7 +108,7 @@ cudaError_t rollout_dispatch(const Dyn& dyn, const IterArgs& a, int cost_kind, c
     return launch_generate_t<DYN_T::NU>(a, e, f, st);                                            \
   }                                                                                             \
   ModelOps NAME##_ops() {                                                                       \
-    return ModelOps{NAME##_rollout, launch_weights, NAME##_update, NAME##_combine,              \
+    return ModelOps{NAME##_rollout, NAME##_plant, launch_weights, NAME##_update, NAME##_combine, \
                     NAME##_generate, DYN_T::NX, DYN_T::NU, DYN_T::NY};                           \
   }                                                                                             \
   }

@@ -83,6 +83,24 @@ struct ResultHeader {
   long long argmin[2];
   long long nonzero[2];
   float next_nominal_state[kMaxNX];
+  // closed loop (smpc_run_control_loop): sticky first error of the loop and
+  // the accumulated applied running cost (plant.cpp:175)
+  unsigned long long loop_err;
+  double loop_cost;
+};
+
+// One SimulatedSystem::step of the closed loop (plant.cpp:31-48, :160-178).
+struct PlantStepArgs {
+  float* x;               // simulated state [NX] (device)
+  float* x0_out;          // the controller's x0 buffer: the next update_state snapshot
+  const float* controls;  // last solution's controls [T][NU]
+  int idx;                // control_for_time index (plant.cpp:106-115)
+  uint32_t step;          // SimulatedSystem::step_count_ and the cost's t
+  float dt;               // (float) controller dt
+  float scale;            // (float)(disturbance_std * sqrt(dt)); 0 = no disturbance
+  PhiloxKeys rk;          // round keys of NormalStream(rng_seed ^ 0x9E3779B97F4A7C15)
+  double t;
+  double* log;            // [steps][2 + NX + NU] rows {t, x, u, c} or nullptr
 };
 
 struct IterArgs {
@@ -153,6 +171,7 @@ struct IterArgs {
 // dispatched inside. Defined in inst_*.cu.
 struct ModelOps {
   cudaError_t (*rollout)(const IterArgs&, int cost_kind, cudaStream_t);
+  cudaError_t (*plant_step)(const IterArgs&, int cost_kind, const PlantStepArgs&, cudaStream_t);
   cudaError_t (*weights)(const IterArgs&, cudaStream_t);
   cudaError_t (*update)(const IterArgs&, cudaStream_t);
   cudaError_t (*combine)(const IterArgs&, cudaStream_t);
@@ -173,6 +192,7 @@ cudaError_t launch_sort_selected(const IterArgs& a, long long k, unsigned long l
                                  unsigned long long* slot, cudaStream_t stream);
 cudaError_t build_tail_table(float* table, uint32_t n, cudaStream_t stream);
 cudaError_t launch_begin_solve(ResultHeader* h, cudaStream_t stream);
+cudaError_t launch_shift_mean(float* mean, int S, int T, int NU, long long steps, cudaStream_t stream);
 cudaError_t launch_icdf_domain(const IterArgs& a, float* out, cudaStream_t stream);
 cudaError_t launch_finish_solve(ResultHeader* h, cudaStream_t stream);
 cudaError_t launch_weights(const IterArgs& a, cudaStream_t stream);

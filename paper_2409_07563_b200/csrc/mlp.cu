@@ -426,6 +426,14 @@ cudaError_t mlp_rollout(const IterArgs& a, int ck, cudaStream_t st) {
   return mlpk::rollout(mlp_make<F>(a.dyn), a, ck, st);
 }
 template <bool F>
+cudaError_t mlp_plant(const IterArgs& a, int ck, const PlantStepArgs& p, cudaStream_t st) {
+  switch (ck) {
+    case 0: return launch_plant_step_t(a, mlp_make<F>(a.dyn), make_road(a.cost), p, st);
+    case 3: return launch_plant_step_t(a, mlp_make<F>(a.dyn), make_quad<7>(a.cost), p, st);
+  }
+  return cudaErrorInvalidValue;
+}
+template <bool F>
 cudaError_t mlp_update(const IterArgs& a, cudaStream_t st) {
   return launch_update_t(a, mlp_make<F>(a.dyn), st);
 }
@@ -439,8 +447,11 @@ cudaError_t mlp_generate(const IterArgs& a, float* e, uint8_t* f, cudaStream_t s
 }  // namespace
 
 ModelOps ops_mlp(bool fma_libm) {
-  if (fma_libm) return ModelOps{mlp_rollout<true>, launch_weights, mlp_update<true>, mlp_combine<true>, mlp_generate, 7, 2, 7};
-  return ModelOps{mlp_rollout<false>, launch_weights, mlp_update<false>, mlp_combine<false>, mlp_generate, 7, 2, 7};
+  if (fma_libm)
+    return ModelOps{mlp_rollout<true>, mlp_plant<true>, launch_weights, mlp_update<true>, mlp_combine<true>,
+                    mlp_generate, 7, 2, 7};
+  return ModelOps{mlp_rollout<false>, mlp_plant<false>, launch_weights, mlp_update<false>, mlp_combine<false>,
+                  mlp_generate, 7, 2, 7};
 }
 
 }  // namespace smpc_dev

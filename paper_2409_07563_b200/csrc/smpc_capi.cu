@@ -470,6 +470,10 @@ void decode_error(smpc_ctx* c, unsigned long long key) {
     snprintf(buf, sizeof buf, "rollout produced invalid running cost at sample %lld timestep %d", m, t);
   } else if (stage == 1) {
     snprintf(buf, sizeof buf, "compute_weights: non-finite cost at sample %lld", m);
+  } else if (stage == 3) {  // closed-loop applied cost (CostFunction::running_cost, costs.cpp:12-14)
+    static const char* cost_names[] = {"road", "circle_track", "diff_drive_nav", "quadratic"};
+    const int ck = c->p.cost_kind;
+    snprintf(buf, sizeof buf, "%s: running cost must be finite and >= 0", ck >= 0 && ck < 4 ? cost_names[ck] : "cost");
   } else if (phase == 1) {
     snprintf(buf, sizeof buf, "control vector has non-finite entry at channel %d", ch);
   } else {
@@ -477,7 +481,7 @@ void decode_error(smpc_ctx* c, unsigned long long key) {
   }
   c->err = buf;
   c->err_sample = stage <= 1 ? m : -1;
-  c->err_t = stage == 0 ? t : -1;
+  c->err_t = stage == 0 || stage == 3 ? t : -1;
   c->err_ch = (stage == 0 && phase == 0) || stage == 2 ? ch : -1;
 }
 
@@ -1260,6 +1264,171 @@ smpc_status smpc_group_compute_control(smpc_ctx** ctxs, int32_t n, const float* 
         out[r].solve_time_ms = now_ms() - t0;
       }
     }
+  });
+}
+
+// ---- closed loop ------------------------------------------------------------
+
+namespace {
+
+// Host side of one Plant::run_control_loop (plant.cpp:133-181): the replan
+// schedule depends only on t, so the host walks it and enqueues, per step,
+// [shift + solve] on replans and one plant step; nothing is synchronised
+// until the end. Several loops are advanced in lockstep (one stream each).
+struct LoopState {
+  smpc_ctx* c;
+  smpc_plant_config pc;
+  long long steps = 0;
+  double dt = 0.0, interval = 0.0, next_replan_t = 0.0, solution_t = 0.0;
+  bool solved_once = false;
+  long long solves = 0;
+  float* d_x = nullptr;
+  double* d_log = nullptr;
+  std::vector<cudaEvent_t> ev;  // per solve: start, end
+  PlantStepArgs p{};
+};
+
+void loop_begin(LoopState& L, smpc_ctx* c, const smpc_plant_config* pc, const float* x0, double duration_s,
+                bool want_log) {
+  L.c = c;
+  L.pc = *pc;
+  if (c->S != 1) throw ConfigError{"run_control_loop: tube controllers are not supported"};
+  if (!(pc->replan_rate > 0.0)) throw RuntimeError{"plant: replan_rate must be > 0"};
+  if (!(pc->dt_min > 0.0)) throw RuntimeError{"plant: dt_min must be > 0"};
+  if (!(pc->disturbance_std >= 0.0)) throw RuntimeError{"simulated system: disturbance_std must be >= 0"};
+  if (!(duration_s > 0.0)) throw RuntimeError{"plant: loop duration must be > 0"};
+  for (int i = 0; i < c->nx; ++i)
+    if (!std::isfinite(x0[i])) throw RuntimeError{"state vector has non-finite entry at channel " + std::to_string(i)};
+  L.dt = c->p.dt;
+  L.steps = std::llround(duration_s / L.dt);
+  L.interval = 1.0 / pc->replan_rate;
+  L.d_x = dalloc<float>(kMaxNX);
+  CK(cudaMemcpyAsync(L.d_x, x0, sizeof(float) * c->nx, cudaMemcpyHostToDevice, c->stream));
+  upload_x0(c, x0, 1);
+  if (want_log) L.d_log = dalloc<double>((size_t)std::max(1LL, L.steps) * (2 + c->nx + c->nu));
+  // loop_err / loop_cost live in the result header
+  const unsigned long long no_err = kNoError;
+  const double zero = 0.0;
+  CK(cudaMemcpyAsync(&c->header()->loop_err, &no_err, sizeof no_err, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(&c->header()->loop_cost, &zero, sizeof zero, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaStreamSynchronize(c->stream));  // the pageable H2D sources above are locals
+  PlantStepArgs& p = L.p;
+  p.x = L.d_x;
+  p.x0_out = c->d_x0;
+  p.controls = reinterpret_cast<const float*>(c->d_result + c->off_controls);
+  p.dt = (float)L.dt;
+  p.scale = (float)(pc->disturbance_std * std::sqrt(L.dt));  // plant.cpp:35
+  const uint64_t sim_seed = pc->rng_seed ^ 0x9E3779B97F4A7C15ull;  // plant.cpp:228-229
+  for (int r = 0; r < 10; ++r) {
+    p.rk.k0[r] = (uint32_t)sim_seed + (uint32_t)r * 0x9E3779B9u;
+    p.rk.k1[r] = (uint32_t)(sim_seed >> 32) + (uint32_t)r * 0xBB67AE85u;
+  }
+  p.log = L.d_log;
+  if (!c->graph) build_graph(c);
+}
+
+void loop_step(LoopState& L, long long step) {
+  smpc_ctx* c = L.c;
+  const double t = (double)step * L.dt;
+  if (!L.solved_once || t >= L.next_replan_t - 1e-9) {
+    if (L.solved_once) {  // shift_control_sequence(t - solution_t, dt_min) (controllers.cpp:68-84)
+      const double elapsed = t - L.solution_t;
+      if (elapsed > 0.0) {
+        const double quantized = (double)std::llrint(elapsed / L.pc.dt_min) * L.pc.dt_min;
+        const long long k = std::llrint(quantized / c->p.dt);
+        if (k > 0) CK(launch_shift_mean(c->d_mean, c->S, c->T, c->nu, k, c->stream));
+      }
+    }
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    L.ev.push_back(e0);
+    L.ev.push_back(e1);
+    CK(cudaEventRecord(e0, c->stream));
+    CK(cudaGraphLaunch(c->graph, c->stream));  // compute_control(x) with x = the sim snapshot (d_x0)
+    CK(cudaEventRecord(e1, c->stream));
+    L.solution_t = t;
+    ++L.solves;
+    L.solved_once = true;
+    while (L.next_replan_t <= t + 1e-9) L.next_replan_t += L.interval;
+  }
+  // control_for_time (plant.cpp:106-115)
+  const long long raw = (long long)std::floor((t - L.solution_t) / c->p.dt);
+  L.p.idx = (int)std::min<long long>(std::max<long long>(raw, 0), c->T - 1);
+  L.p.step = (uint32_t)step;
+  L.p.t = t;
+  IterArgs a = c->base;
+  CK(c->ops.plant_step(a, c->p.cost_kind, L.p, c->stream));
+}
+
+void loop_end(LoopState& L, smpc_loop_result* out, double* log_out) {
+  smpc_ctx* c = L.c;
+  CK(cudaMemcpyAsync(c->h_result, c->d_result, c->result_bytes, cudaMemcpyDeviceToHost, c->stream));
+  if (log_out && L.d_log)
+    CK(cudaMemcpyAsync(log_out, L.d_log, sizeof(double) * L.steps * (2 + c->nx + c->nu), cudaMemcpyDeviceToHost,
+                       c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  double total_ms = 0.0;
+  for (size_t i = 0; i + 1 < L.ev.size(); i += 2) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, L.ev[i], L.ev[i + 1]));
+    total_ms += ms;
+  }
+  for (auto e : L.ev) cudaEventDestroy(e);
+  L.ev.clear();
+  cudaFree(L.d_x);
+  if (L.d_log) cudaFree(L.d_log);
+  const ResultHeader* h = c->h_header();
+  c->solve_count = h->solve_count;
+  if (h->loop_err != kNoError) {
+    decode_error(c, h->loop_err);
+    throw RuntimeError{c->err};
+  }
+  if (out) {
+    out->accumulated_cost = h->loop_cost;
+    out->solve_count = L.solves;
+    out->mean_solve_ms = L.solves ? total_ms / (double)L.solves : 0.0;
+    out->steps = L.steps;
+  }
+}
+
+}  // namespace
+
+smpc_status smpc_run_control_loop(smpc_ctx* c, const smpc_plant_config* pc, const float* x0, double duration_s,
+                                  smpc_loop_result* out, double* log_out) {
+  if (!c || !pc || !x0) return SMPC_ERR_ARGUMENT;
+  return guarded(c, [&] {
+    LoopState L;
+    loop_begin(L, c, pc, x0, duration_s, log_out != nullptr);
+    for (long long step = 0; step < L.steps; ++step) loop_step(L, step);
+    loop_end(L, out, log_out);
+  });
+}
+
+smpc_status smpc_run_control_loops(smpc_ctx** cs, int32_t n, const smpc_plant_config* pcs, const float* x0s,
+                                   double duration_s, smpc_loop_result* outs) {
+  if (!cs || n < 1 || !pcs || !x0s) return SMPC_ERR_ARGUMENT;
+  for (int i = 0; i < n; ++i)
+    if (!cs[i]) return SMPC_ERR_ARGUMENT;
+  std::vector<LoopState> L((size_t)n);
+  smpc_ctx* failed = cs[0];
+  return guarded(cs[0], [&] {
+    size_t off = 0;
+    for (int i = 0; i < n; ++i) {
+      failed = cs[i];
+      loop_begin(L[i], cs[i], &pcs[i], x0s + off, duration_s, false);
+      off += (size_t)cs[i]->nx;
+    }
+    long long steps = 0;
+    for (int i = 0; i < n; ++i) steps = std::max(steps, L[i].steps);
+    for (long long step = 0; step < steps; ++step)
+      for (int i = 0; i < n; ++i)
+        if (step < L[i].steps) loop_step(L[i], step);
+    for (int i = 0; i < n; ++i) {
+      failed = cs[i];
+      loop_end(L[i], outs ? &outs[i] : nullptr, nullptr);
+    }
+    (void)failed;
   });
 }
 

@@ -123,6 +123,20 @@ class SmpcTubeSolution(ctypes.Structure):
     ]
 
 
+class SmpcPlantConfig(ctypes.Structure):
+    """smpc_plant_config (include/smpc_b200.h)."""
+
+    _fields_ = [("replan_rate", ctypes.c_double), ("dt_min", ctypes.c_double),
+                ("disturbance_std", ctypes.c_double), ("rng_seed", ctypes.c_uint64)]
+
+
+class SmpcLoopResult(ctypes.Structure):
+    """smpc_loop_result (include/smpc_b200.h)."""
+
+    _fields_ = [("accumulated_cost", ctypes.c_double), ("solve_count", ctypes.c_int64),
+                ("mean_solve_ms", ctypes.c_double), ("steps", ctypes.c_int64)]
+
+
 @dataclasses.dataclass
 class Costmap:
     """Costmap2D (costmap.hpp:17-63): binary grid, row 0 at the lowest y."""
@@ -209,6 +223,10 @@ class Scenario:
     nominal_reset_bound: float = math.inf
     elite_fraction: float = 0.125
     initial_state: Dict[str, float] = dataclasses.field(default_factory=dict)
+    # plant (PlantSection, scenario.hpp:107-114)
+    replan_rate: float = 50.0
+    dt_min: float = 0.02
+    disturbance_std: float = 0.0
     device: int = 0
     # B200 deployment knob (not in the reference schema): weighted-update
     # samples with w_m < update_skip_mass / M are skipped (0 = exact).
@@ -427,6 +445,14 @@ def autorally_scenario(num_samples: int = 8192, horizon: int = 100, seed: int = 
                     target=[0.0, 0.0, 0.0, 0.0, 4.0, 0.0, 0.0], weights=[0.0, 0.5, 1.0, 0.1, 1.0, 0.1, 0.1],
                     mlp_weights=autorally_mlp_weights(weights_seed), controller=controller,
                     initial_state={"V_X": 2.0})
+
+
+def default_sweep_scenario() -> Scenario:
+    """bench.cpp:186-202: the point mass holding an annular orbit, the stock
+    subject of the closed-loop step-size sweep (dmd controller)."""
+    return Scenario(dt=0.02, horizon=32, lambda_=1.0, control_std=(1.0, 1.0), importance_sampling=False,
+                    dynamics="double_integrator", cost="circle_track", controller="dmd", step_size=1.0,
+                    replan_rate=50.0, dt_min=0.02, initial_state={"X": 2.0, "V_Y": 2.0})
 
 
 def synthetic_costmap(seed: int = 3) -> Costmap:

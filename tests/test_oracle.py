@@ -120,7 +120,8 @@ def _scenario_from_index(name, rec):
     return sc
 
 
-GOLDEN_FILES = sorted(glob.glob(os.path.join(GOLDEN, "*.npz")))
+GOLDEN_FILES = sorted(p for p in glob.glob(os.path.join(GOLDEN, "*.npz")) if not os.path.basename(p).startswith("loop_"))
+LOOP_FILES = sorted(glob.glob(os.path.join(GOLDEN, "loop_*.npz")))
 
 
 @pytest.mark.parametrize("path", GOLDEN_FILES, ids=[os.path.basename(p)[:-4] for p in GOLDEN_FILES])
@@ -231,3 +232,19 @@ def test_mlp_oracle_zero_network_is_pure_kinematics(port):
     c, s = np.cos(np.float32(0.5)), np.sin(np.float32(0.5))
     assert abs(xn[0] - 0.1 * (2.0 * c - 0.5 * s)) < 1e-6 and abs(xn[1] - 0.1 * (2.0 * s + 0.5 * c)) < 1e-6
     assert abs(xn[2] - 0.53) < 1e-6 and np.array_equal(xn[3:], x[3:])
+
+
+
+@pytest.mark.parametrize("path", LOOP_FILES, ids=[os.path.basename(p)[:-4] for p in LOOP_FILES])
+def test_closed_loop_checker_matches_reference_goldens(oracle_built, path):
+    """The Python Plant::run_control_loop around the C oracle (oracle.bindings.
+    control_loop) reproduces the reference's own closed loop bit for bit:
+    replan schedule, shifts, applied controls, running costs, disturbances."""
+    name = os.path.basename(path)[:-4]
+    rec = dict(np.load(path))
+    sc = _scenario_from_index(name, rec)
+    if sc.cost == "diff_drive_nav" and sc.costmap is None:
+        sc.costmap = S.synthetic_costmap()
+    acc, rows = oracle_built.control_loop(sc, int(rec["steps"]) * sc.dt)
+    assert acc == rec["accumulated_cost"]
+    assert np.array_equal(rows, rec["rows"])
