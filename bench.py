@@ -11,7 +11,7 @@ samples, T = 100 (the large-sample sweep config the metric is quoted on for
 with the WorkerPool chunk rule).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--workload di|cartpole|diffdrive|quadrotor|autorally] [--samples N]
+                  [--workload di|cartpole|diffdrive|quadrotor|autorally|bicycle] [--samples N]
                   [--scaling strong|weak]
 
 Rank 0 prints ONE JSON line. `value` = samples/s of the whole job from
@@ -44,8 +44,12 @@ from paper_2409_07563_b200 import scenario as S  # noqa: E402
 # autorally (C4, Tube S=2; per system-sample-step): SIMT layers 1 and 3 =
 # (6x32 + 32x4) MACs = 640 FP32 ops + 64 tanh, noise 2x29, kinematics 6,
 # Euler 14; tensor layer 2 = 32x32 MACs = 2048 flops (3xTF32 issues 3x that).
-FP32_OPS_PER_SAMPLE_STEP = {"di": 83, "cartpole": 56, "diffdrive": 90, "quadrotor": 214, "autorally": 718}
-FP64_OPS_PER_SAMPLE_STEP = {"di": 9, "cartpole": 23, "diffdrive": 19, "quadrotor": 65, "autorally": 41}
+# bicycle (C3, Ackermann): noise 58, control+clamp 6, derivative 5 (+4 sin/cos),
+# Euler 6, wrap 2, nav cost 16.
+FP32_OPS_PER_SAMPLE_STEP = {"di": 83, "cartpole": 56, "diffdrive": 90, "quadrotor": 214, "autorally": 718,
+                            "bicycle": 93}
+FP64_OPS_PER_SAMPLE_STEP = {"di": 9, "cartpole": 23, "diffdrive": 19, "quadrotor": 65, "autorally": 41,
+                            "bicycle": 19}
 TENSOR_FLOPS_PER_SAMPLE_STEP = {"autorally": 2048}
 # workloads whose model exists in the reference (oracle/_ref can time them)
 REFERENCE_WORKLOADS = ("di", "cartpole", "diffdrive")
@@ -60,6 +64,8 @@ def make_scenario(workload: str, n: int) -> S.Scenario:
         return S.diff_drive_nav_scenario(num_samples=n, horizon=56, seed=42)
     if workload == "quadrotor":
         return S.quadrotor_scenario(num_samples=n, horizon=100, seed=13)
+    if workload == "bicycle":
+        return S.bicycle_nav_scenario(num_samples=n, horizon=56, seed=42)
     if workload == "autorally":
         return S.autorally_scenario(num_samples=n, horizon=100, seed=21, controller="tube")
     raise SystemExit(f"unknown workload {workload}")
@@ -70,7 +76,8 @@ def workload_name(workload: str, n: int) -> str:
             "cartpole": f"C1 cartpole+quadratic MPPI N={n} T=100",
             "diffdrive": f"C3 diff_drive+diff_drive_nav(costmap 110x110) MPPI N={n} T=56",
             "quadrotor": f"C2 quadrotor(13-state)+quadratic tracking MPPI N={n} T=100",
-            "autorally": f"C4 AutoRally MLP dynamics (tcgen05) Tube-MPPI N={n} T=100"}[workload]
+            "autorally": f"C4 AutoRally MLP dynamics (tcgen05) Tube-MPPI N={n} T=100",
+            "bicycle": f"C3 Ackermann/bicycle+diff_drive_nav(costmap 110x110) MPPI N={n} T=56"}[workload]
 
 
 class ClockSampler:
@@ -363,7 +370,8 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="di", choices=["di", "cartpole", "diffdrive", "quadrotor", "autorally"])
+    ap.add_argument("--workload", default="di", choices=["di", "cartpole", "diffdrive", "quadrotor", "autorally",
+                                                           "bicycle"])
     ap.add_argument("--samples", type=int, default=1 << 20)
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
     ap.add_argument("--roofline-steps", type=int, default=20)

@@ -137,6 +137,9 @@ int oracle_dims_of(const smpc_problem* p, oracle_dims* d, oracle_error* err) {
     case SMPC_DYN_QUADROTOR:
       d->n_x = 13, d->n_u = 4, d->n_y = 13;
       return 0;
+    case SMPC_DYN_BICYCLE:
+      d->n_x = 3, d->n_u = 2, d->n_y = 3;
+      return 0;
     case SMPC_DYN_MLP:
       if (!p->dyn_tensor || p->dyn_tensor_len != 1412) return fail(err, "mlp: dyn_tensor must hold 1412 floats");
       d->n_x = 7, d->n_u = 2, d->n_y = 7;
@@ -269,6 +272,13 @@ static void state_derivative(const smpc_problem* p, const float* x, const float*
     case SMPC_DYN_MLP:
       mlp_derivative(p, x, u, dx);
       break;
+    case SMPC_DYN_BICYCLE: { /* builder-defined kinematic bicycle (device twin: models.cuh BicycleDyn) */
+      dx[0] = u[0] * cosf(x[2]);
+      dx[1] = u[0] * sinf(x[2]);
+      const float tan_d = sinf(u[1]) / cosf(u[1]);
+      dx[2] = (u[0] * tan_d) / (float)dparam(p, 0, 0.5);
+      break;
+    }
   }
 }
 
@@ -280,6 +290,15 @@ static void clamp_control(const smpc_problem* p, const float* u, float* out, int
     for (int i = 0; i < 2; ++i) {
       const float a = u[i] < lo[i] ? lo[i] : u[i]; /* std::max(u, lo) */
       out[i] = hi[i] < a ? hi[i] : a;              /* std::min(., hi) */
+    }
+    return;
+  }
+  if (p->dynamics_kind == SMPC_DYN_BICYCLE) {
+    const float lo[2] = {(float)dparam(p, 1, -0.35), (float)dparam(p, 3, -0.6)};
+    const float hi[2] = {(float)dparam(p, 2, 0.5), (float)dparam(p, 4, 0.6)};
+    for (int i = 0; i < 2; ++i) {
+      const float a = u[i] < lo[i] ? lo[i] : u[i];
+      out[i] = hi[i] < a ? hi[i] : a;
     }
     return;
   }

@@ -185,6 +185,7 @@ ModelOps ops_diff_drive(bool fma_libm);
 ModelOps ops_double_integrator();
 ModelOps ops_quadrotor();
 ModelOps ops_mlp(bool fma_libm);
+ModelOps ops_bicycle(bool fma_libm);
 
 cudaError_t launch_select(const IterArgs& a, SelectState* st, long long k, unsigned int* counters, int* eq_cnt,
                           long long* eq_off, cudaStream_t stream);

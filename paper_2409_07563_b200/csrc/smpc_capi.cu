@@ -225,6 +225,14 @@ void validate(smpc_ctx* c) {
         throw RuntimeError{"quadrotor: thrust_max must exceed hover thrust and rate_max must be > 0"};
       c->ops = ops_quadrotor();
       break;
+    case SMPC_DYN_BICYCLE:  // builder-defined (models.cuh:BicycleDyn)
+      if (!((float)pd(p, 0, 0.5) > 0.0f)) throw RuntimeError{"bicycle: wheelbase must be > 0"};
+      if (!((float)pd(p, 1, -0.35) < (float)pd(p, 2, 0.5)))
+        throw RuntimeError{"bicycle: control bound lower must be < upper on channel 0"};
+      if (!((float)pd(p, 3, -0.6) < (float)pd(p, 4, 0.6)))
+        throw RuntimeError{"bicycle: control bound lower must be < upper on channel 1"};
+      c->ops = ops_bicycle(c->fma);
+      break;
     case SMPC_DYN_MLP:  // builder-defined (models.cuh:MlpDyn, tcgen05 rollout in mlp.cu)
       if (!p.dyn_tensor || p.dyn_tensor_len != mlp_layout::TOTAL)
         throw RuntimeError{"mlp: dyn_tensor must hold " + std::to_string(mlp_layout::TOTAL) +
@@ -271,7 +279,8 @@ void validate(smpc_ctx* c) {
       break;
     default: throw ConfigError{"cost.kind is not recognized"};
   }
-  static const char* dyn_names[] = {"unicycle", "cartpole", "diff_drive", "double_integrator", "quadrotor", "mlp"};
+  static const char* dyn_names[] = {"unicycle", "cartpole", "diff_drive", "double_integrator", "quadrotor", "mlp",
+                                    "bicycle"};
   if (cost_ny != c->ny)
     throw ConfigError{"cost '" + cost_name + "' expects " + std::to_string(cost_ny) +
                       " output channels but model '" + dyn_names[p.dynamics_kind] + "' produces " +
@@ -389,6 +398,11 @@ void fill_args(smpc_ctx* c) {
     case SMPC_DYN_DIFF_DRIVE: {
       const double d[6] = {1.0, 1.0, -0.35, 0.5, -0.5, 0.5};
       for (int i = 0; i < 6; ++i) a.dyn.p[i] = (float)pd(p, i, d[i]);
+      break;
+    }
+    case SMPC_DYN_BICYCLE: {
+      const double d[5] = {0.5, -0.35, 0.5, -0.6, 0.6};
+      for (int i = 0; i < 5; ++i) a.dyn.p[i] = (float)pd(p, i, d[i]);
       break;
     }
     case SMPC_DYN_QUADROTOR: {

@@ -23,7 +23,7 @@ ABI_VERSION = 2
 
 DYNAMICS_KINDS = {"unicycle": 0, "cartpole": 1, "diff_drive": 2, "double_integrator": 3,
                   # builder-defined (no reference counterpart): BASELINE.json configs[1] / configs[3]
-                  "quadrotor": 4, "mlp": 5}
+                  "quadrotor": 4, "mlp": 5, "bicycle": 6}
 COST_KINDS = {"road": 0, "circle_track": 1, "diff_drive_nav": 2, "quadratic": 3}
 CONTROLLER_KINDS = {"mppi": 0, "dmd": 1, "cem": 2, "tube": 3}
 
@@ -36,6 +36,7 @@ MODEL_DIMS = {
     "double_integrator": (4, 2, 4),
     "quadrotor": (13, 4, 13),
     "mlp": (7, 2, 7),
+    "bicycle": (3, 2, 3),
 }
 STATE_NAMES = {
     "unicycle": ["X", "Y", "YAW"],
@@ -46,6 +47,7 @@ STATE_NAMES = {
     # AutoRally state convention (MPPI-Generic AutoRallyDynamics): pose, then the
     # body-frame dynamic state the network predicts
     "mlp": ["X", "Y", "YAW", "ROLL", "V_X", "V_Y", "YAW_RATE"],
+    "bicycle": ["X", "Y", "YAW"],
 }
 
 
@@ -259,6 +261,9 @@ class Scenario:
         if self.dynamics == "diff_drive":
             return [d.get("wheel_radius", 1.0), d.get("wheel_length", 1.0), d.get("v_min", -0.35),
                     d.get("v_max", 0.5), d.get("w_min", -0.5), d.get("w_max", 0.5)]
+        if self.dynamics == "bicycle":
+            return [d.get("wheelbase", 0.5), d.get("v_min", -0.35), d.get("v_max", 0.5),
+                    d.get("steer_min", -0.6), d.get("steer_max", 0.6)]
         if self.dynamics == "quadrotor":
             return [d.get("mass", 1.0), d.get("gravity", 9.81), d.get("rate_time_constant", 0.05),
                     d.get("thrust_max", 39.24), d.get("rate_max", 5.0)]
@@ -400,6 +405,17 @@ def di_swarm_scenario(num_samples: int = 1 << 20, horizon: int = 100, seed: int 
     return Scenario(num_samples=num_samples, horizon=horizon, dt=0.02, lambda_=1.0, control_std=(1.0, 1.0),
                     rng_seed=seed, importance_sampling=False, dynamics="double_integrator",
                     cost="circle_track", initial_state={"X": 2.0, "V_Y": 2.0})
+
+
+def bicycle_nav_scenario(num_samples: int = 2000, horizon: int = 56, seed: int = 42,
+                         costmap: Optional[Costmap] = None) -> Scenario:
+    """C3: kinematic bicycle / Ackermann vehicle on the synthetic 11 m x 11 m
+    costmap with the diff_drive_nav cost (BASELINE.json configs[2], the Nav2
+    comparison workload; builder-defined model, see models.cuh:BicycleDyn)."""
+    return Scenario(num_samples=num_samples, horizon=horizon, dt=0.02, lambda_=1.0, control_std=(0.2, 0.3),
+                    rng_seed=seed, dynamics="bicycle", cost="diff_drive_nav",
+                    costmap=costmap if costmap is not None else synthetic_costmap(),
+                    initial_state={"X": -2.0, "Y": -2.0})
 
 
 def quadrotor_scenario(num_samples: int = 8192, horizon: int = 100, seed: int = 13) -> Scenario:

@@ -48,6 +48,8 @@ def scenarios(S):
                                control_std=(0.7, 0.4), controller="dmd", step_size=0.6, lambda_=2.0),
         # BASELINE.json configs[1]: builder-defined 13-state quadrotor (restated oracle only)
         "quadrotor": S.quadrotor_scenario(num_samples=1024, horizon=100, seed=13),
+        # BASELINE.json configs[2]: builder-defined kinematic bicycle on the synthetic costmap
+        "bicycle_nav": S.bicycle_nav_scenario(num_samples=2000, horizon=56, seed=42),
     }
 
 
@@ -83,7 +85,7 @@ def test_icdf_whole_domain_bit_exact(mods):
 
 
 @pytest.mark.parametrize("name", ["cartpole", "double_integrator", "diff_drive_nav", "unicycle_road",
-                                  "cartpole_road_perstep", "di_quadratic_dmd", "quadrotor"])
+                                  "cartpole_road_perstep", "di_quadratic_dmd", "quadrotor", "bicycle_nav"])
 def test_generate_samples_bit_exact(mods, name):
     sc = scenarios(mods["S"])[name]
     n_x, n_u, n_y = sc.dims
@@ -96,7 +98,7 @@ def test_generate_samples_bit_exact(mods, name):
 
 
 @pytest.mark.parametrize("name", ["cartpole", "double_integrator", "diff_drive_nav", "unicycle_road",
-                                  "cartpole_road_perstep", "di_quadratic_dmd", "quadrotor"])
+                                  "cartpole_road_perstep", "di_quadratic_dmd", "quadrotor", "bicycle_nav"])
 @pytest.mark.parametrize("systems", [1, 2])
 def test_rollout_costs_bit_exact(mods, name, systems):
     """Fused rollout (Philox regenerated in-kernel and injected noise) vs oracle:
@@ -138,7 +140,7 @@ def test_compute_weights_matches_oracle(mods):
 
 
 @pytest.mark.parametrize("name", ["cartpole", "double_integrator", "diff_drive_nav", "unicycle_road",
-                                  "cartpole_road_perstep", "di_quadratic_dmd", "quadrotor"])
+                                  "cartpole_road_perstep", "di_quadratic_dmd", "quadrotor", "bicycle_nav"])
 def test_compute_control_matches_oracle(mods, name):
     """Three warm-started solves: rho and argmin exact, U*/states/weights within 1e-4."""
     sc = scenarios(mods["S"])[name]

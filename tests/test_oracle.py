@@ -248,3 +248,16 @@ def test_closed_loop_checker_matches_reference_goldens(oracle_built, path):
     acc, rows = oracle_built.control_loop(sc, int(rec["steps"]) * sc.dt)
     assert acc == rec["accumulated_cost"]
     assert np.array_equal(rows, rec["rows"])
+
+
+def test_bicycle_oracle_kinematics(port):
+    """Builder-defined kinematic bicycle: straight line at zero steering, yaw
+    rate v tan(delta) / L, controls clamped to the configured bounds."""
+    sc = S.bicycle_nav_scenario(num_samples=4, horizon=5)
+    x = np.array([0.0, 0.0, 0.0], np.float32)
+    xn, _ = port.step(sc, x, np.array([0.4, 0.0], np.float32), np.float32(0.1))
+    assert np.allclose(xn, [0.04, 0.0, 0.0], atol=1e-7)
+    xn, _ = port.step(sc, x, np.array([0.4, 0.3], np.float32), np.float32(0.1))
+    assert abs(xn[2] - 0.1 * 0.4 * np.tan(0.3) / 0.5) < 1e-6
+    xn, _ = port.step(sc, x, np.array([9.0, 9.0], np.float32), np.float32(0.1))  # clamped to (0.5, 0.6)
+    assert abs(xn[0] - 0.05) < 1e-7 and abs(xn[2] - 0.1 * 0.5 * np.tan(0.6) / 0.5) < 1e-6
