@@ -21,7 +21,7 @@ EXPORTED = [
     "smpc_create", "smpc_destroy", "smpc_last_error", "smpc_error_location", "smpc_get_dims",
     "smpc_set_mean", "smpc_get_mean", "smpc_compute_control", "smpc_tube_compute_control",
     "smpc_shift_control_sequence", "smpc_get_solve_count", "smpc_set_solve_count",
-    "smpc_generate_samples", "smpc_rollout", "smpc_compute_weights", "smpc_sorted_samples", "smpc_run_control_loop", "smpc_run_control_loops", "smpc_set_x0",
+    "smpc_generate_samples", "smpc_rollout", "smpc_compute_weights", "smpc_sorted_samples", "smpc_export_sample_trajectories", "smpc_run_control_loop", "smpc_run_control_loops", "smpc_set_x0",
     "smpc_launch_iteration", "smpc_synchronize", "smpc_stream", "smpc_kernels_per_solve",
     "smpc_rollout_kernel_ms", "smpc_icdf_domain", "smpc_comm_unique_id", "smpc_comm_init", "smpc_group_init",
     "smpc_group_compute_control", "smpc_host_libm_uses_fma",
@@ -83,6 +83,9 @@ def load(path: str = None) -> ctypes.CDLL:
                                          ctypes.c_void_p]
     L.smpc_run_control_loops.argtypes = [P(c_ctx), ctypes.c_int32, P(SmpcPlantConfig), f32p, ctypes.c_double,
                                           P(SmpcLoopResult)]
+    L.smpc_export_sample_trajectories.argtypes = [c_ctx, f32p, f32p, ctypes.c_void_p, ctypes.c_uint32,
+                                                  ctypes.c_double, P(ctypes.c_int64), ctypes.c_void_p,
+                                                  ctypes.c_void_p]
     L.smpc_set_x0.argtypes = [c_ctx, f32p]
     L.smpc_launch_iteration.argtypes = [c_ctx]
     L.smpc_synchronize.argtypes = [c_ctx]
@@ -105,7 +108,7 @@ def load(path: str = None) -> ctypes.CDLL:
     for name in ["smpc_create", "smpc_error_location", "smpc_get_dims", "smpc_set_mean", "smpc_get_mean",
                  "smpc_compute_control", "smpc_tube_compute_control", "smpc_shift_control_sequence",
                  "smpc_get_solve_count", "smpc_set_solve_count", "smpc_generate_samples", "smpc_rollout",
-                 "smpc_compute_weights", "smpc_sorted_samples", "smpc_run_control_loop", "smpc_run_control_loops", "smpc_set_x0", "smpc_launch_iteration", "smpc_synchronize",
+                 "smpc_compute_weights", "smpc_sorted_samples", "smpc_export_sample_trajectories", "smpc_run_control_loop", "smpc_run_control_loops", "smpc_set_x0", "smpc_launch_iteration", "smpc_synchronize",
                  "smpc_rollout_kernel_ms", "smpc_icdf_domain", "smpc_comm_unique_id", "smpc_comm_init", "smpc_group_init",
                  "smpc_group_compute_control"]:
         getattr(L, name).restype = ctypes.c_int

@@ -116,6 +116,20 @@ class RolloutEngine(_Context):
             return costs, outs.reshape(S, self.M_local, self.T, self.n_y)
         return costs
 
+    def export_sample_trajectories(self, x0, mean, fraction: float, eps=None, stream: int = 0):
+        """RolloutEngine::export_sample_trajectories (engine.cpp:411-455): the
+        ceil(fraction*M) lowest-cost samples (cost, index order) of the rollout
+        of (x0, mean, eps | Philox stream) and their [k, T, n_y] outputs."""
+        k_max = int(np.ceil(fraction * self.M)) if 0.0 <= fraction <= 1.0 else 0
+        order = np.zeros(max(k_max, 1), np.int64)
+        outs = np.zeros(max(k_max, 1) * self.T * self.n_y, np.float32)
+        k = ctypes.c_int64()
+        e = _f32(eps).reshape(-1) if eps is not None else None
+        self._check(self.lib.smpc_export_sample_trajectories(
+            self.ctx, _f32(x0).ravel(), _f32(mean).ravel(), e.ctypes.data if e is not None else None, stream,
+            float(fraction), ctypes.byref(k), order.ctypes.data, outs.ctypes.data))
+        return order[:k.value], outs[:k.value * self.T * self.n_y].reshape(k.value, self.T, self.n_y)
+
     def compute_weights(self, costs, lam: float) -> WeightResult:
         costs = np.ascontiguousarray(costs, np.float64).ravel()
         w = np.zeros_like(costs)

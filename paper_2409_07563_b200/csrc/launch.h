@@ -163,6 +163,9 @@ struct IterArgs {
   int normalize_weights;  // write w = e/eta back (only when the caller wants weights)
   double skip_w;          // update skips samples with w_m < skip_w (0 = exact)
   double cem_k;           // CEM: elite count k (commit mean + acc / k); 0 = MPPI / Tube
+  // Indexed rollout (export_sample_trajectories re-roll): thread i rolls out
+  // global sample sample_idx[i] (nullptr: m_begin + i)
+  const long long* sample_idx;
   DynParams dyn;
   CostParams cost;
 };

@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(kTile, 4) mlp_rollout_kernel(const IterArgs a,
 
   const int i = blockIdx.x * kTile + tid;
   const bool active = i < a.M_local;
-  const long long m = a.m_begin + i;
+  const long long m = (a.sample_idx && active) ? a.sample_idx[i] : a.m_begin + i;
   const bool is_mean = a.with_mean && m == 0;
   const bool zero_mean = m >= a.zero_begin;
   const uint32_t stream = noise_stream(a);
@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(kTile, 4) mlp_rollout_kernel(const IterArgs a,
       const int k = t * NU + c;
       float e;
       if constexpr (INJ) {
-        e = active ? a.eps_in[(size_t)i * TU + k] : 0.0f;
+        e = active ? a.eps_in[(size_t)(m - a.m_begin) * TU + k] : 0.0f;
       } else {
         if ((k & 3) == 0) zq = normal_quad_fast(a, stream, (uint32_t)m, (uint32_t)(k >> 2));
         float ev = F_MUL(sigma_s[k], quad_lane(zq, k & 3));

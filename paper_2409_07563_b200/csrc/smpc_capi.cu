@@ -363,6 +363,7 @@ void fill_args(smpc_ctx* c) {
   a.sig2 = c->d_sig2;
   a.gamma = c->d_gamma;
   a.eps_in = nullptr;
+  a.sample_idx = nullptr;
   a.tail = c->d_tail;
   a.costs = c->d_costs;
   a.outputs = nullptr;
@@ -1178,6 +1179,80 @@ smpc_status smpc_sorted_samples(smpc_ctx* c, int32_t system, int64_t count, int6
         const unsigned long long b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
         memcpy(&costs_out[i], &b, sizeof b);
       }
+    }
+  });
+}
+
+smpc_status smpc_export_sample_trajectories(smpc_ctx* c, const float* x0, const float* mean, const float* eps,
+                                            uint32_t stream, double fraction, int64_t* k_out, int64_t* order_out,
+                                            float* outputs_out) {
+  if (!c || !x0 || !mean || !k_out) return SMPC_ERR_ARGUMENT;
+  return guarded(c, [&] {
+    if (!(fraction >= 0.0 && fraction <= 1.0)) throw RuntimeError{"export_sample_trajectories: fraction must be in [0, 1]"};
+    if (c->world > 1 || c->M_local != c->M) throw ConfigError{"export_sample_trajectories: single-shard contexts only"};
+    const long long k = (long long)std::ceil(fraction * (double)c->M);  // engine.cpp:417
+    *k_out = k;
+    if (k == 0) return;
+    const size_t TU = (size_t)c->T * c->nu;
+    if (!c->d_ro_mean) c->d_ro_mean = dalloc<float>(2 * TU);
+    if (!c->d_ro_x0) c->d_ro_x0 = dalloc<float>(2 * kMaxNX);
+    CK(cudaMemcpyAsync(c->d_ro_mean, mean, sizeof(float) * TU, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->d_ro_x0, x0, sizeof(float) * c->nx, cudaMemcpyHostToDevice, c->stream));
+    IterArgs a = c->base;
+    a.S = 1;
+    a.solve_count = nullptr;
+    a.stream = stream;
+    a.iter = 0;
+    a.mean_in = c->d_ro_mean;
+    a.x0 = c->d_ro_x0;
+    a.rank = 0;
+    a.world = 1;
+    if (eps) {
+      const size_t n = (size_t)c->M_local * TU;
+      if (c->eps_cap < n) {
+        if (c->d_eps) cudaFree(c->d_eps);
+        c->d_eps = dalloc<float>(n);
+        c->eps_cap = n;
+      }
+      CK(cudaMemcpyAsync(c->d_eps, eps, sizeof(float) * n, cudaMemcpyHostToDevice, c->stream));
+      a.eps_in = c->d_eps;
+    }
+    // 1) the fused rollout (RolloutResult::costs, system 0)
+    CK(launch_begin_solve(c->header(), c->stream));
+    CK(c->ops.rollout(a, c->p.cost_kind, c->stream));
+    // 2) the k lowest (cost, index) samples in partial_sort order (engine.cpp:419-426)
+    long long n_pad = 1;
+    while (n_pad < k) n_pad <<= 1;
+    unsigned long long* keys = dalloc<unsigned long long>((size_t)n_pad + 1);
+    long long* idx = dalloc<long long>((size_t)n_pad);
+    CK(launch_select(a, c->d_select, k, c->d_counters + 8, c->d_eq_cnt, c->d_eq_off, c->stream));
+    CK(launch_sort_selected(a, k, keys, idx, keys + n_pad, c->stream));
+    // 3) re-roll just the chosen samples with stored outputs (engine.cpp:435-453)
+    float* outs = dalloc<float>((size_t)k * c->T * c->ny);
+    double* costs = dalloc<double>((size_t)k);
+    const int nblk = (int)((k + kRolloutThreads - 1) / kRolloutThreads);
+    double* bmin = dalloc<double>((size_t)nblk);
+    long long* barg = dalloc<long long>((size_t)nblk);
+    IterArgs b = a;
+    b.sample_idx = idx;
+    b.M_local = (int)k;
+    b.costs = costs;
+    b.outputs = outs;
+    b.n_roll_blocks = nblk;
+    b.blk_min = bmin;
+    b.blk_arg = barg;
+    CK(c->ops.rollout(b, c->p.cost_kind, c->stream));
+    ResultHeader h;
+    if (order_out) CK(cudaMemcpyAsync(order_out, idx, sizeof(long long) * k, cudaMemcpyDeviceToHost, c->stream));
+    if (outputs_out)
+      CK(cudaMemcpyAsync(outputs_out, outs, sizeof(float) * k * c->T * c->ny, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(&h, c->header(), sizeof h, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    void* tmp[] = {keys, idx, outs, costs, bmin, barg};
+    for (void* q : tmp) cudaFree(q);
+    if (h.err_key != kNoError && (h.err_key >> 62) == 0) {
+      decode_error(c, h.err_key);
+      throw RuntimeError{c->err};
     }
   });
 }
