@@ -82,6 +82,10 @@ class Oracle:
             L.oracle_partial_sort.argtypes = [_f64p, ctypes.c_int64, ctypes.c_int64,
                                               np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS")]
             L.oracle_clamp_control.argtypes = [ctypes.POINTER(SmpcProblem), _f32p, _f32p]
+            L.oracle_rmppi_compute_control.argtypes = [
+                ctypes.POINTER(SmpcProblem), _f32p, _f32p, ctypes.POINTER(ctypes.c_int32),
+                ctypes.POINTER(ctypes.c_uint64), _f32p, _f32p, _f32p, _f32p, _f32p, ctypes.POINTER(ctypes.c_int32),
+                ctypes.POINTER(SmpcWeightSummary), ctypes.POINTER(_OracleErr)]
             L.oracle_wrap_angle.argtypes = [ctypes.c_float]
             L.oracle_wrap_angle.restype = ctypes.c_float
             L.oracle_angular_channel.argtypes = [ctypes.POINTER(SmpcProblem)]
@@ -324,6 +328,28 @@ class OracleController:
                            solve_time_ms=s4[3])
         return dict(controls=controls.reshape(T, n_u), states=states.reshape(T + 1, n_x),
                     outputs=outputs.reshape(T, n_y), weights=weights, **summary)
+
+    def rmppi_compute_control(self, x_real):
+        """Builder-defined RMPPI solve on the C oracle (port only)."""
+        sc = self.sc
+        n_x, n_u, n_y = sc.dims
+        T = sc.horizon
+        x_real = np.ascontiguousarray(x_real, np.float32)
+        ctl = np.zeros(T * n_u, np.float32)
+        ns = np.zeros((T + 1) * n_x, np.float32)
+        rs = np.zeros((T + 1) * n_x, np.float32)
+        chosen = np.zeros(n_x, np.float32)
+        choice = ctypes.c_int32()
+        sm = SmpcWeightSummary()
+        err = _OracleErr()
+        rc = self.o.lib.oracle_rmppi_compute_control(
+            ctypes.byref(self.problem), self.mean, self.nominal_state, ctypes.byref(self.nominal_started),
+            ctypes.byref(self.solve_count), x_real, ctl, ns, rs, chosen, ctypes.byref(choice), ctypes.byref(sm),
+            ctypes.byref(err))
+        Oracle._check(rc, err.message)
+        return dict(controls=ctl.reshape(T, n_u), nominal_states=ns.reshape(T + 1, n_x),
+                    real_states=rs.reshape(T + 1, n_x), nominal_state=chosen, choice=choice.value,
+                    baseline=sm.baseline, normalizer=sm.normalizer, argmin=sm.argmin)
 
     def tube_compute_control(self, x_real):
         sc = self.sc

@@ -821,6 +821,143 @@ void oracle_clamp_control(const smpc_problem* p, const float* u, float* out) {
 float oracle_wrap_angle(float a) { return wrap_angle(a); }
 int oracle_angular_channel(const smpc_problem* p) { return angular_channel(p); }
 
+/* ---- RMPPI (builder-defined: PAPER.md:150-151; device twin smpc_capi.cu /
+ * kernels.cuh rmppi_select_kernel + the S = 2 rollout with feedback) ------- */
+
+/* DynamicsModel::interpolate_states (dynamics.cpp:106-120). */
+static void interpolate_states(const smpc_problem* p, const oracle_dims* d, const float* a, const float* b,
+                               float alpha, float* out) {
+  const int ang = angular_channel(p);
+  for (int i = 0; i < d->n_x; ++i) out[i] = a[i] + alpha * (b[i] - a[i]);
+  if (ang >= 0) out[ang] = wrap_angle(a[ang] + alpha * wrap_angle(b[ang] - a[ang]));
+}
+
+/* Cost of the mean rolled out from z (running + terminal; non-finite -> inf). */
+static double mean_trajectory_cost(const smpc_problem* p, const oracle_dims* d, const float* z, const float* mean) {
+  float x[KMAX], xn[KMAX], y[KMAX];
+  memcpy(x, z, sizeof(float) * d->n_x);
+  double total = 0.0;
+  for (int t = 0; t < p->horizon; ++t) {
+    step_raw(p, d, x, &mean[(size_t)t * d->n_u], (float)p->dt, xn, y);
+    total += running_cost(p, y);
+    memcpy(x, xn, sizeof(float) * d->n_x);
+  }
+  const double J = total + terminal_cost(p, y);
+  return J == J ? J : INFINITY;
+}
+
+int oracle_rmppi_compute_control(const smpc_problem* p, float* mean, float* nominal_state,
+                                 int32_t* nominal_started, uint64_t* solve_count, const float* x_real,
+                                 float* controls, float* nominal_states, float* real_states,
+                                 float* chosen_nominal, int32_t* choice, smpc_weight_summary* summary,
+                                 oracle_error* err) {
+  oracle_dims d;
+  if (oracle_dims_of(p, &d, err)) return SMPC_ERR_CONFIG;
+  const int M = p->num_samples, T = p->horizon, n_u = d.n_u, n_x = d.n_x;
+  const size_t K = (size_t)T * n_u;
+  float prev[KMAX], z[KMAX];
+  memcpy(prev, *nominal_started ? nominal_state : x_real, sizeof(float) * n_x);
+  *nominal_started = 1;
+  /* candidate nominal states: the largest i with J(z_i) <= alpha, else i = 0 */
+  const int n = p->num_candidates;
+  int best = 0;
+  for (int i = n - 1; i > 0; --i) {
+    interpolate_states(p, &d, prev, x_real, (float)i / (float)(n - 1), z);
+    if (mean_trajectory_cost(p, &d, z, mean) <= p->cost_threshold) {
+      best = i;
+      break;
+    }
+  }
+  interpolate_states(p, &d, prev, x_real, n > 1 ? (float)best / (float)(n - 1) : 1.0f, z);
+  if (chosen_nominal) memcpy(chosen_nominal, z, sizeof(float) * n_x);
+  if (choice) *choice = best;
+  float* eps = (float*)malloc(sizeof(float) * (size_t)M * K);
+  double* costs = (double*)malloc(sizeof(double) * 2 * (size_t)M);
+  double* adj = (double*)malloc(sizeof(double) * (size_t)M);
+  double* w = (double*)malloc(sizeof(double) * (size_t)M);
+  float* updated = (float*)malloc(sizeof(float) * K);
+  const float dt = (float)p->dt;
+  int rc = 0;
+  smpc_weight_summary sm = {0};
+  for (int iter = 0; !rc && iter < p->iterations; ++iter) {
+    const uint32_t stream = (uint32_t)(*solve_count * 256u + (uint64_t)iter);
+    rc = oracle_generate_samples(p, mean, 0, M, stream, eps, NULL, err);
+    if (rc) break;
+    oracle_importance(p, eps, M, mean, adj); /* both systems sample about the one mean */
+    /* coupled rollout: first failure in (system, sample, timestep) order */
+    int fail_s = 2, fail_ch = -1, fail_t = -1, fail_kind = 0;
+    int64_t fail_m = -1;
+    for (int64_t m = 0; m < M; ++m) {
+      float xs[2][KMAX], xn[KMAX], y[2][KMAX], u[2][KMAX];
+      memcpy(xs[0], z, sizeof(float) * n_x);
+      memcpy(xs[1], x_real, sizeof(float) * n_x);
+      double total[2] = {0.0, 0.0};
+      int dead[2] = {0, 0};
+      for (int t = 0; t < T; ++t) {
+        const float* e = &eps[((size_t)m * T + t) * n_u];
+        for (int c = 0; c < n_u; ++c) {
+          float fb = 0.0f;
+          if (p->feedback_gain)
+            for (int j = 0; j < n_x; ++j) fb += p->feedback_gain[c * n_x + j] * (xs[1][j] - xs[0][j]);
+          u[0][c] = mean[(size_t)t * n_u + c] + e[c];
+          u[1][c] = u[0][c] + fb;
+        }
+        for (int s = 0; s < 2; ++s) {
+          step_raw(p, &d, xs[s], u[s], dt, xn, y[s]);
+          const double ct = running_cost(p, y[s]);
+          if (!dead[s]) {
+            int ch = -1;
+            for (int c = n_x - 1; c >= 0; --c)
+              if (!isfinite(xn[c])) ch = c;
+            if (ch >= 0 || !(ct >= 0.0 && isfinite(ct))) {
+              dead[s] = 1;
+              if (s < fail_s || (s == fail_s && m < fail_m)) {
+                fail_s = s, fail_m = m, fail_t = t, fail_ch = ch, fail_kind = ch >= 0 ? 0 : 1;
+              }
+            }
+          }
+          total[s] += ct;
+          memcpy(xs[s], xn, sizeof(float) * n_x);
+        }
+      }
+      for (int s = 0; s < 2; ++s) {
+        double J = total[s] + terminal_cost(p, y[s]);
+        if (p->importance_sampling) J += adj[m];
+        costs[(size_t)s * M + m] = J;
+      }
+    }
+    if (fail_s < 2) {
+      rc = rollout_error(err, fail_kind ? "invalid running cost" : NULL, fail_kind ? -1 : fail_ch, fail_m, fail_t);
+      break;
+    }
+    /* one control sequence, updated with the real (feedback) system's weights */
+    rc = oracle_compute_weights(&costs[M], M, p->lambda, w, &sm.baseline, &sm.normalizer, &sm.argmin, err);
+    if (rc) break;
+    int64_t nz = 0;
+    for (int m = 0; m < M; ++m) nz += w[m] != 0.0;
+    sm.nonzero = nz;
+    rc = oracle_weighted_update(mean, T, n_u, eps, M, w, p->step_sizes, p->n_step_sizes, updated, err);
+    if (rc) break;
+    memcpy(mean, updated, sizeof(float) * K);
+  }
+  free(eps);
+  free(costs);
+  free(adj);
+  free(w);
+  free(updated);
+  if (rc) return rc;
+  ++*solve_count;
+  if (summary) *summary = sm;
+  if (controls) memcpy(controls, mean, sizeof(float) * K);
+  rc = finish_solution(p, &d, mean, z, nominal_states, NULL, err);
+  if (!rc) rc = finish_solution(p, &d, mean, x_real, real_states, NULL, err);
+  if (rc) return rc;
+  float xn[KMAX], y[KMAX];
+  step_raw(p, &d, z, mean, dt, xn, y); /* the nominal system advances through the model */
+  memcpy(nominal_state, xn, sizeof(float) * n_x);
+  return 0;
+}
+
 /* CostFunction::running_cost_raw / terminal_cost_raw (costs.hpp:24-25) for unit tests. */
 double oracle_running_cost(const smpc_problem* p, const float* y) { return running_cost(p, y); }
 double oracle_terminal_cost(const smpc_problem* p, const float* y) { return terminal_cost(p, y); }

@@ -260,8 +260,8 @@ class TubeMppiController(MppiController):
 
 
 def make_controller(scenario: Scenario, shard: Optional[tuple] = None) -> MppiController:
-    """make_controller (controllers.cpp:294-344): mppi | dmd | cem | tube."""
-    if scenario.controller == "tube":
+    """make_controller (controllers.cpp:294-344): mppi | dmd | cem | tube (+ rmppi, builder-defined)."""
+    if scenario.controller in ("tube", "rmppi"):
         return TubeMppiController(scenario, shard)
     if scenario.controller in ("mppi", "dmd", "cem"):
         return MppiController(scenario, shard)

@@ -71,6 +71,24 @@ cudaError_t rollout_dispatch(const Dyn& dyn, const IterArgs& a, int cost_kind, c
 }
 
 template <class Dyn>
+cudaError_t rmppi_dispatch(const Dyn& dyn, const IterArgs& a, int cost_kind, cudaStream_t st) {
+  switch (cost_kind) {
+    case 0:
+      if constexpr (Dyn::NY >= 2) return launch_rmppi_select_t(a, dyn, make_road(a.cost), st);
+      break;
+    case 1:
+      if constexpr (Dyn::NY == 4 && Dyn::NU == 2) return launch_rmppi_select_t(a, dyn, make_circle(a.cost), st);
+      break;
+    case 2:
+      if constexpr (Dyn::NY == 3 && Dyn::NU == 2) return launch_rmppi_select_t(a, dyn, make_nav(a.cost), st);
+      break;
+    case 3:
+      return launch_rmppi_select_t(a, dyn, make_quad<Dyn::NY>(a.cost), st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <class Dyn>
 cudaError_t plant_dispatch(const Dyn& dyn, const IterArgs& a, int cost_kind, const PlantStepArgs& p,
                            cudaStream_t st) {
   switch (cost_kind) {
@@ -95,6 +113,9 @@ cudaError_t plant_dispatch(const Dyn& dyn, const IterArgs& a, int cost_kind, con
   cudaError_t NAME##_rollout(const IterArgs& a, int ck, cudaStream_t st) {                       \
     return rollout_dispatch(NAME##_make(a.dyn), a, ck, st);                                      \
   }                                                                                             \
+  cudaError_t NAME##_rmppi(const IterArgs& a, int ck, cudaStream_t st) {                          \
+    return rmppi_dispatch(NAME##_make(a.dyn), a, ck, st);                                        \
+  }                                                                                             \
   cudaError_t NAME##_plant(const IterArgs& a, int ck, const PlantStepArgs& p, cudaStream_t st) {   \
     return plant_dispatch(NAME##_make(a.dyn), a, ck, p, st);                                     \
   }                                                                                             \
@@ -108,7 +129,7 @@ cudaError_t plant_dispatch(const Dyn& dyn, const IterArgs& a, int cost_kind, con
     return launch_generate_t<DYN_T::NU>(a, e, f, st);                                            \
   }                                                                                             \
   ModelOps NAME##_ops() {                                                                       \
-    return ModelOps{NAME##_rollout, NAME##_plant, launch_weights, NAME##_update, NAME##_combine, \
+    return ModelOps{NAME##_rollout, NAME##_rmppi, NAME##_plant, launch_weights, NAME##_update, NAME##_combine, \
                     NAME##_generate, DYN_T::NX, DYN_T::NU, DYN_T::NY};                           \
   }                                                                                             \
   }

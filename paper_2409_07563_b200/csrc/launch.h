@@ -83,6 +83,9 @@ struct ResultHeader {
   long long argmin[2];
   long long nonzero[2];
   float next_nominal_state[kMaxNX];
+  // RMPPI: the nominal state chosen for this solve and its candidate index
+  float rmppi_nominal[kMaxNX];
+  int rmppi_choice;
   // closed loop (smpc_run_control_loop): sticky first error of the loop and
   // the accumulated applied running cost (plant.cpp:175)
   unsigned long long loop_err;
@@ -163,6 +166,14 @@ struct IterArgs {
   int normalize_weights;  // write w = e/eta back (only when the caller wants weights)
   double skip_w;          // update skips samples with w_m < skip_w (0 = exact)
   double cem_k;           // CEM: elite count k (commit mean + acc / k); 0 = MPPI / Tube
+  // RMPPI (S = 2): the real system's sampled control gets the ancillary
+  // feedback u += K (x_real,t - x_nominal,t) of the same sample; candidate
+  // nominal states z_i on the segment previous-nominal -> real (x0[0] ->
+  // x0[1] on entry) are scored by their mean-trajectory cost.
+  int rmppi;
+  float fb_gain[kMaxNU * kMaxNX];  // K, row-major [NU][NX]
+  int n_cand;
+  double cost_threshold;
   // Indexed rollout (export_sample_trajectories re-roll): thread i rolls out
   // global sample sample_idx[i] (nullptr: m_begin + i)
   const long long* sample_idx;
@@ -174,6 +185,7 @@ struct IterArgs {
 // dispatched inside. Defined in inst_*.cu.
 struct ModelOps {
   cudaError_t (*rollout)(const IterArgs&, int cost_kind, cudaStream_t);
+  cudaError_t (*rmppi_select)(const IterArgs&, int cost_kind, cudaStream_t);
   cudaError_t (*plant_step)(const IterArgs&, int cost_kind, const PlantStepArgs&, cudaStream_t);
   cudaError_t (*weights)(const IterArgs&, cudaStream_t);
   cudaError_t (*update)(const IterArgs&, cudaStream_t);

@@ -448,9 +448,9 @@ cudaError_t mlp_generate(const IterArgs& a, float* e, uint8_t* f, cudaStream_t s
 
 ModelOps ops_mlp(bool fma_libm) {
   if (fma_libm)
-    return ModelOps{mlp_rollout<true>, mlp_plant<true>, launch_weights, mlp_update<true>, mlp_combine<true>,
+    return ModelOps{mlp_rollout<true>, nullptr, mlp_plant<true>, launch_weights, mlp_update<true>, mlp_combine<true>,
                     mlp_generate, 7, 2, 7};
-  return ModelOps{mlp_rollout<false>, mlp_plant<false>, launch_weights, mlp_update<false>, mlp_combine<false>,
+  return ModelOps{mlp_rollout<false>, nullptr, mlp_plant<false>, launch_weights, mlp_update<false>, mlp_combine<false>,
                   mlp_generate, 7, 2, 7};
 }
 

@@ -90,14 +90,18 @@ T* dalloc(size_t n) {
 }
 
 const char* controller_name(int kind) {
-  return kind == SMPC_CTRL_DMD ? "dmd" : kind == SMPC_CTRL_TUBE ? "tube" : kind == SMPC_CTRL_CEM ? "cem" : "mppi";
+  return kind == SMPC_CTRL_DMD     ? "dmd"
+         : kind == SMPC_CTRL_TUBE  ? "tube"
+         : kind == SMPC_CTRL_CEM   ? "cem"
+         : kind == SMPC_CTRL_RMPPI ? "rmppi"
+                                   : "mppi";
 }
 
 }  // namespace
 
 struct smpc_ctx {
   smpc_problem p{};
-  std::vector<float> std_per_step, step_sizes;
+  std::vector<float> std_per_step, step_sizes, fb_gain;
   std::vector<uint8_t> costmap;
   ModelOps ops{};
   int nx = 0, nu = 0, ny = 0, S = 1, T = 0, I = 1;
@@ -245,7 +249,7 @@ void validate(smpc_ctx* c) {
   }
   c->nx = c->ops.nx, c->nu = c->ops.nu, c->ny = c->ops.ny;
   if (p.controller_kind != SMPC_CTRL_MPPI && p.controller_kind != SMPC_CTRL_DMD &&
-      p.controller_kind != SMPC_CTRL_TUBE && p.controller_kind != SMPC_CTRL_CEM)
+      p.controller_kind != SMPC_CTRL_TUBE && p.controller_kind != SMPC_CTRL_CEM && p.controller_kind != SMPC_CTRL_RMPPI)
     throw ConfigError{"controller.kind is not recognized"};
   // cost (make_cost + ctor checks)
   int cost_ny = c->ny, cost_nu = c->nu;
@@ -312,6 +316,14 @@ void validate(smpc_ctx* c) {
       throw RuntimeError{name + ": step sizes must be in (0, 1]"};
   if (p.controller_kind == SMPC_CTRL_TUBE && !(p.nominal_reset_bound > 0.0))
     throw RuntimeError{"tube: nominal_reset_bound must be > 0"};
+  if (p.controller_kind == SMPC_CTRL_RMPPI) {
+    if (!c->ops.rmppi_select) throw ConfigError{"rmppi: not supported for this dynamics model"};
+    if (p.num_candidates < 2 || p.num_candidates > 32) throw RuntimeError{"rmppi: num_candidates must be in [2, 32]"};
+    if (p.cost_threshold != p.cost_threshold) throw RuntimeError{"rmppi: cost_threshold must not be NaN"};
+    if (p.feedback_gain)
+      for (int k = 0; k < c->nu * c->nx; ++k)
+        if (!std::isfinite(p.feedback_gain[k])) throw RuntimeError{"rmppi: feedback gains must be finite"};
+  }
   if (p.controller_kind == SMPC_CTRL_CEM && !(p.elite_fraction > 0.0 && p.elite_fraction <= 1.0))
     throw RuntimeError{"cem: elite_fraction must be in (0, 1]"};  // controllers.cpp:145-147
   if (!(p.update_skip_mass >= 0.0 && p.update_skip_mass < 1e-6))
@@ -351,6 +363,11 @@ void fill_args(smpc_ctx* c) {
   // CEM ranks raw rollout costs: no importance adjustment (controllers.cpp:155-162).
   a.importance = p.importance_sampling != 0 && p.controller_kind != SMPC_CTRL_CEM;
   a.cem_k = p.controller_kind == SMPC_CTRL_CEM ? (double)c->cem_k : 0.0;
+  a.rmppi = p.controller_kind == SMPC_CTRL_RMPPI;
+  for (int k = 0; k < kMaxNU * kMaxNX; ++k) a.fb_gain[k] = 0.0f;
+  for (size_t k = 0; k < c->fb_gain.size(); ++k) a.fb_gain[k] = c->fb_gain[k];
+  a.n_cand = p.num_candidates;
+  a.cost_threshold = p.cost_threshold;
   a.world = c->world;
   a.rank = c->rank;
   a.solve_count = &c->header()->solve_count;
@@ -503,6 +520,10 @@ void decode_error(smpc_ctx* c, unsigned long long key) {
 // One solve's device work on c->stream (graph-captured or direct).
 void enqueue_solve(smpc_ctx* c, bool timed) {
   CK(launch_begin_solve(c->header(), c->stream));
+  if (c->p.controller_kind == SMPC_CTRL_RMPPI) {  // nominal-state choice, once per solve
+    IterArgs a = c->base;
+    CK(c->ops.rmppi_select(a, c->p.cost_kind, c->stream));
+  }
   for (int it = 0; it < c->I; ++it) {
     IterArgs a = c->base;
     a.iter = it;
@@ -689,7 +710,9 @@ smpc_status smpc_create(const smpc_problem* problem, smpc_ctx** out) {
     c->T = p.horizon;
     c->I = p.iterations;
     c->M = p.num_samples;
-    c->S = p.controller_kind == SMPC_CTRL_TUBE ? 2 : 1;
+    c->S = (p.controller_kind == SMPC_CTRL_TUBE || p.controller_kind == SMPC_CTRL_RMPPI) ? 2 : 1;
+    if (p.feedback_gain) c->fb_gain.assign(p.feedback_gain, p.feedback_gain + (size_t)c->nu * c->nx);
+    p.feedback_gain = nullptr;
     // k = max(1, (int)ceil(elite_fraction * M)) (controllers.cpp:164)
     c->cem_k = std::max(1, (int)std::ceil(p.elite_fraction * (double)p.num_samples));
     c->m_begin = 0;
@@ -859,6 +882,8 @@ smpc_status smpc_set_mean(smpc_ctx* c, int32_t system, const float* mean) {
     for (size_t k = 0; k < TU; ++k)
       if (!std::isfinite(mean[k])) throw RuntimeError{"control vector has non-finite entry at channel " + std::to_string(k % c->nu)};
     CK(cudaMemcpyAsync(c->d_mean + system * TU, mean, sizeof(float) * TU, cudaMemcpyHostToDevice, c->stream));
+    if (c->p.controller_kind == SMPC_CTRL_RMPPI)  // one control sequence, mirrored into both systems
+      CK(cudaMemcpyAsync(c->d_mean + (1 - system) * TU, mean, sizeof(float) * TU, cudaMemcpyHostToDevice, c->stream));
     CK(cudaStreamSynchronize(c->stream));
   });
 }
@@ -919,15 +944,17 @@ smpc_status smpc_tube_compute_control(smpc_ctx* c, const float* x_real, smpc_tub
     set_error(c, "tube_compute_control: context is not a tube controller");
     return SMPC_ERR_RUNTIME;
   }
+  const bool rmppi = c->p.controller_kind == SMPC_CTRL_RMPPI;
   return guarded(c, [&] {
     const double t0 = now_ms();
     for (int i = 0; i < c->nx; ++i)
       if (!std::isfinite(x_real[i])) throw RuntimeError{"state vector has non-finite entry at channel " + std::to_string(i)};
-    // nominal-state bookkeeping (controllers.cpp:221-227)
+    // nominal-state bookkeeping (controllers.cpp:221-227); RMPPI chooses on the
+    // device between the previous nominal state and x_real (rmppi_select_kernel)
     if (!c->nominal_started) {
       c->nominal_state.assign(x_real, x_real + c->nx);
       c->nominal_started = true;
-    } else if (std::isfinite(c->p.nominal_reset_bound)) {
+    } else if (!rmppi && std::isfinite(c->p.nominal_reset_bound)) {
       float acc = 0.f;
       for (int i = 0; i < c->nx; ++i) {
         const float d = x_real[i] - c->nominal_state[i];
@@ -942,6 +969,10 @@ smpc_status smpc_tube_compute_control(smpc_ctx* c, const float* x_real, smpc_tub
     launch_solve(c);
     fetch_results(c);
     const double elapsed = now_ms() - t0;
+    if (rmppi) {
+      const float* z = c->h_header()->rmppi_nominal;
+      c->nominal_state.assign(z, z + c->nx);
+    }
     if (out) {
       if (out->nominal_state) memcpy(out->nominal_state, c->nominal_state.data(), sizeof(float) * c->nx);
       copy_solution(c, 0, &out->nominal);

@@ -19,13 +19,13 @@ import numpy as np
 
 SMPC_MAX_DIM = 16
 SMPC_MAX_PARAMS = 32
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 DYNAMICS_KINDS = {"unicycle": 0, "cartpole": 1, "diff_drive": 2, "double_integrator": 3,
                   # builder-defined (no reference counterpart): BASELINE.json configs[1] / configs[3]
                   "quadrotor": 4, "mlp": 5, "bicycle": 6}
 COST_KINDS = {"road": 0, "circle_track": 1, "diff_drive_nav": 2, "quadratic": 3}
-CONTROLLER_KINDS = {"mppi": 0, "dmd": 1, "cem": 2, "tube": 3}
+CONTROLLER_KINDS = {"mppi": 0, "dmd": 1, "cem": 2, "tube": 3, "rmppi": 4}
 
 # ModelDims per dynamics kind (dynamics.cpp:122-181) and state names
 # (used by initial_state, scenario.hpp:136-137 / state_from_named_values).
@@ -73,6 +73,9 @@ class SmpcProblem(ctypes.Structure):
         ("step_sizes", ctypes.POINTER(ctypes.c_float)),
         ("nominal_reset_bound", ctypes.c_double),
         ("elite_fraction", ctypes.c_double),
+        ("feedback_gain", ctypes.POINTER(ctypes.c_float)),
+        ("cost_threshold", ctypes.c_double),
+        ("num_candidates", ctypes.c_int32),
         ("dynamics_kind", ctypes.c_int32),
         ("n_dyn_params", ctypes.c_int32),
         ("dyn_params", ctypes.c_double * SMPC_MAX_PARAMS),
@@ -224,6 +227,10 @@ class Scenario:
     step_size_per_step: Optional[Sequence[float]] = None
     nominal_reset_bound: float = math.inf
     elite_fraction: float = 0.125
+    # RMPPI (builder-defined, see include/smpc_b200.h SMPC_CTRL_RMPPI)
+    feedback_gain: Optional[Sequence[Sequence[float]]] = None  # K [n_u][n_x]
+    cost_threshold: float = math.inf
+    num_candidates: int = 9
     initial_state: Dict[str, float] = dataclasses.field(default_factory=dict)
     # plant (PlantSection, scenario.hpp:107-114)
     replan_rate: float = 50.0
@@ -322,6 +329,12 @@ class Scenario:
             p.step_sizes = sarr.ctypes.data_as(ctypes.POINTER(ctypes.c_float))
         p.nominal_reset_bound = float(self.nominal_reset_bound)
         p.elite_fraction = float(self.elite_fraction)
+        if self.feedback_gain is not None:
+            kg = np.ascontiguousarray(np.asarray(self.feedback_gain, np.float32).reshape(n_u, n_x))
+            keep.append(kg)
+            p.feedback_gain = kg.ctypes.data_as(ctypes.POINTER(ctypes.c_float))
+        p.cost_threshold = float(self.cost_threshold)
+        p.num_candidates = int(self.num_candidates)
         p.dynamics_kind = DYNAMICS_KINDS[self.dynamics]
         if self.dynamics == "mlp":
             wb = np.ascontiguousarray(self.mlp_weights if self.mlp_weights is not None else autorally_mlp_weights(),
