@@ -1,10 +1,9 @@
-// Kernel instantiations: DiffDriveModel (dynamics.cpp:158-171), control
-// bounds {v_min, w_min} / {v_max, w_max} from params [2..5].
+// Kernel instantiations: DiffDriveModel (dynamics.cpp:158-171), glibc sinf/cosf generic ifunc
+// variant (one variant per translation unit so the two compile in parallel).
 #include "inst_common.cuh"
 
 namespace smpc_dev {
-#define SMPC_DD(F) return DiffDriveDyn<F>{{p.p[2], p.p[4]}, {p.p[3], p.p[5]}};
-SMPC_DEFINE_OPS(dd_fma, DiffDriveDyn<true>, SMPC_DD(true))
-SMPC_DEFINE_OPS(dd_gen, DiffDriveDyn<false>, SMPC_DD(false))
-ModelOps ops_diff_drive(bool fma_libm) { return fma_libm ? dd_fma_ops() : dd_gen_ops(); }
+SMPC_DEFINE_OPS(dd_gen, DiffDriveDyn<false>, return DiffDriveDyn<false>{{p.p[2], p.p[4]}, {p.p[3], p.p[5]}};)
+ModelOps dd_fma_ops_ext();
+ModelOps ops_diff_drive(bool fma_libm) { return fma_libm ? dd_fma_ops_ext() : dd_gen_ops(); }
 }  // namespace smpc_dev
