@@ -23,6 +23,10 @@ constexpr int TOTAL = B3 + OUT;  // 1412
 
 constexpr int kUpdateThreads = 256;
 constexpr int kUpdateWarps = kUpdateThreads / 32;
+#ifndef SMPC_UPDATE_MIN_BLOCKS2
+#define SMPC_UPDATE_MIN_BLOCKS2 2
+#endif
+constexpr int kUpdateCtasPerSm = SMPC_UPDATE_MIN_BLOCKS2;  // resident update CTAs per SM (QPL = 2 bound)
 
 // Error key (lowest key wins = what a single-worker reference would throw):
 //   [63:62] stage  0 rollout, 1 compute_weights, 2 finish_solution

@@ -740,7 +740,14 @@ smpc_status smpc_create(const smpc_problem* problem, smpc_ctx** out) {
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     c->n_roll_blocks = (int)((c->M_local + kRolloutThreads - 1) / kRolloutThreads);
     c->n_w_blocks = (int)std::min<long long>((c->M_local + 255) / 256, 148 * 4);
-    c->n_u_blocks = (int)std::max<long long>(1, std::min<long long>((c->M_local + 255) / 256, 148 * 4));
+    // update grid: one wave of the update kernel's resident CTAs (kUpdateCtasPerSm per SM)
+    {
+      int sms = 148;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p.device);
+      int per_sm = kUpdateCtasPerSm;
+      if (const char* e = getenv("SMPC_UPDATE_CTAS_PER_SM")) per_sm = std::max(1, atoi(e));  // A/B knob
+      c->n_u_blocks = (int)std::max<long long>(1, std::min<long long>((c->M_local + 255) / 256, (long long)sms * per_sm));
+    }
 
     c->d_mean = dalloc<float>((size_t)c->S * TU);
     c->d_x0 = dalloc<float>((size_t)2 * kMaxNX);
