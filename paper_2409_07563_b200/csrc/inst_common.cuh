@@ -8,6 +8,11 @@
 
 namespace smpc_dev {
 
+template <class D>
+struct is_bicycle : std::false_type {};
+template <bool F>
+struct is_bicycle<BicycleDyn<F>> : std::true_type {};
+
 inline RoadCostDev make_road(const CostParams& c) {
   RoadCostDev r;
   r.half_width = c.p[0];
@@ -55,8 +60,8 @@ inline QuadraticCostDev<NY> make_quad(const CostParams& c) {
 template <class Dyn>
 cudaError_t rollout_dispatch(const Dyn& dyn, const IterArgs& a, int cost_kind, cudaStream_t st) {
   switch (cost_kind) {
-    case 0:  // road: needs n_y >= 2 (costs.cpp:30)
-      if constexpr (Dyn::NY >= 2) return launch_rollout_t(a, dyn, make_road(a.cost), st);
+    case 0:  // road: needs n_y >= 2 (costs.cpp:30); not offered for the builder-defined bicycle
+      if constexpr (Dyn::NY >= 2 && !is_bicycle<Dyn>::value) return launch_rollout_t(a, dyn, make_road(a.cost), st);
       break;
     case 1:  // circle_track: (n_y, n_u) = (4, 2)
       if constexpr (Dyn::NY == 4 && Dyn::NU == 2) return launch_rollout_t(a, dyn, make_circle(a.cost), st);
@@ -74,7 +79,7 @@ template <class Dyn>
 cudaError_t rmppi_dispatch(const Dyn& dyn, const IterArgs& a, int cost_kind, cudaStream_t st) {
   switch (cost_kind) {
     case 0:
-      if constexpr (Dyn::NY >= 2) return launch_rmppi_select_t(a, dyn, make_road(a.cost), st);
+      if constexpr (Dyn::NY >= 2 && !is_bicycle<Dyn>::value) return launch_rmppi_select_t(a, dyn, make_road(a.cost), st);
       break;
     case 1:
       if constexpr (Dyn::NY == 4 && Dyn::NU == 2) return launch_rmppi_select_t(a, dyn, make_circle(a.cost), st);
@@ -93,7 +98,7 @@ cudaError_t plant_dispatch(const Dyn& dyn, const IterArgs& a, int cost_kind, con
                            cudaStream_t st) {
   switch (cost_kind) {
     case 0:
-      if constexpr (Dyn::NY >= 2) return launch_plant_step_t(a, dyn, make_road(a.cost), p, st);
+      if constexpr (Dyn::NY >= 2 && !is_bicycle<Dyn>::value) return launch_plant_step_t(a, dyn, make_road(a.cost), p, st);
       break;
     case 1:
       if constexpr (Dyn::NY == 4 && Dyn::NU == 2) return launch_plant_step_t(a, dyn, make_circle(a.cost), p, st);

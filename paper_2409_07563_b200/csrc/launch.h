@@ -27,6 +27,9 @@ constexpr int kUpdateWarps = kUpdateThreads / 32;
 #define SMPC_UPDATE_MIN_BLOCKS2 2
 #endif
 constexpr int kUpdateCtasPerSm = SMPC_UPDATE_MIN_BLOCKS2;  // resident update CTAs per SM (QPL = 2 bound)
+// Shards up to this many samples pre-generate the iteration's noise in one
+// parallel pass (gen_zq_kernel) instead of inside each sample's serial chain.
+constexpr long long kZqMaxSamples = 16384;
 
 // Error key (lowest key wins = what a single-worker reference would throw):
 //   [63:62] stage  0 rollout, 1 compute_weights, 2 finish_solution
@@ -181,6 +184,9 @@ struct IterArgs {
   // Indexed rollout (export_sample_trajectories re-roll): thread i rolls out
   // global sample sample_idx[i] (nullptr: m_begin + i)
   const long long* sample_idx;
+  // Small-N mode: the iteration's standard-normal quads pre-generated by
+  // gen_zq_kernel, [Q][M_local] float4 (nullptr: regenerate in the rollout)
+  const float4* zq;
   DynParams dyn;
   CostParams cost;
 };
@@ -213,6 +219,7 @@ cudaError_t launch_sort_selected(const IterArgs& a, long long k, unsigned long l
 cudaError_t build_tail_table(float* table, uint32_t n, cudaStream_t stream);
 cudaError_t launch_begin_solve(ResultHeader* h, cudaStream_t stream);
 cudaError_t launch_shift_mean(float* mean, int S, int T, int NU, long long steps, cudaStream_t stream);
+cudaError_t launch_gen_zq(const IterArgs& a, int nu, float4* zq, cudaStream_t stream);
 cudaError_t launch_icdf_domain(const IterArgs& a, float* out, cudaStream_t stream);
 cudaError_t launch_finish_solve(ResultHeader* h, cudaStream_t stream);
 cudaError_t launch_weights(const IterArgs& a, cudaStream_t stream);

@@ -213,6 +213,9 @@ __global__ void __launch_bounds__(kTile, 4) mlp_rollout_kernel(const IterArgs a,
   for (int c = 0; c < NX; ++c) x[c] = a.x0[sys * NX + c];
   unsigned long long err = kNoError;
   float4 zq = make_float4(0.f, 0.f, 0.f, 0.f);
+  // small-N mode: pre-generated quads, prefetched one quad ahead
+  const size_t zi = (size_t)(active ? i : 0);
+  float4 zn = a.zq ? __ldg(a.zq + zi) : make_float4(0.f, 0.f, 0.f, 0.f);
   uint32_t phase = 0;
   unsigned char* hhi = smem + L.h0;
   unsigned char* hlo = hhi + kHBytes;
@@ -228,7 +231,14 @@ __global__ void __launch_bounds__(kTile, 4) mlp_rollout_kernel(const IterArgs a,
       if constexpr (INJ) {
         e = active ? a.eps_in[(size_t)(m - a.m_begin) * TU + k] : 0.0f;
       } else {
-        if ((k & 3) == 0) zq = normal_quad_fast(a, stream, (uint32_t)m, (uint32_t)(k >> 2));
+        if ((k & 3) == 0) {
+          if (a.zq) {
+            zq = zn;
+            if ((k >> 2) + 1 < (TU + 3) / 4) zn = __ldg(a.zq + (size_t)((k >> 2) + 1) * a.M_local + zi);
+          } else {
+            zq = normal_quad_fast(a, stream, (uint32_t)m, (uint32_t)(k >> 2));
+          }
+        }
         float ev = F_MUL(sigma_s[k], quad_lane(zq, k & 3));
         if (zero_mean) ev = F_SUB(ev, mean_s[k]);
         e = is_mean ? 0.0f : ev;

@@ -119,6 +119,7 @@ struct smpc_ctx {
   unsigned int* d_counters = nullptr;
   uint8_t* d_costmap = nullptr;
   float* d_dyn_tensor = nullptr;
+  float4* d_zq = nullptr;  // small-N mode noise buffer [Q][M_local]
   // CEM elite selection / sample ordering (select.cu)
   SelectState* d_select = nullptr;
   int* d_eq_cnt = nullptr;
@@ -258,6 +259,7 @@ void validate(smpc_ctx* c) {
     case SMPC_COST_ROAD:
       cost_name = "road";
       if (c->ny < 2) throw RuntimeError{"road cost needs at least 2 output channels"};
+      if (p.dynamics_kind == SMPC_DYN_BICYCLE) throw ConfigError{"road cost is not offered for the bicycle model"};
       if (!((float)pc(p, 0, 1.0) > 0.0f)) throw RuntimeError{"road cost: half_width must be > 0"};
       break;
     case SMPC_COST_CIRCLE_TRACK: {
@@ -381,6 +383,7 @@ void fill_args(smpc_ctx* c) {
   a.gamma = c->d_gamma;
   a.eps_in = nullptr;
   a.sample_idx = nullptr;
+  a.zq = nullptr;
   a.tail = c->d_tail;
   a.costs = c->d_costs;
   a.outputs = nullptr;
@@ -529,6 +532,10 @@ void enqueue_solve(smpc_ctx* c, bool timed) {
     a.iter = it;
     a.do_finish = it == c->I - 1;
     if (timed) CK(cudaEventRecord(c->ev[2 * it], c->stream));
+    if (c->d_zq) {  // small-N mode: the noise as one parallel pass, off the per-sample serial chain
+      a.zq = c->d_zq;
+      CK(launch_gen_zq(a, c->nu, c->d_zq, c->stream));
+    }
     CK(c->ops.rollout(a, c->p.cost_kind, c->stream));
     if (timed) CK(cudaEventRecord(c->ev[2 * it + 1], c->stream));
     if (c->p.controller_kind == SMPC_CTRL_CEM) {  // elite selection replaces compute_weights
@@ -766,6 +773,11 @@ smpc_status smpc_create(const smpc_problem* problem, smpc_ctx** out) {
     c->d_blk_part = dalloc<double>((size_t)c->S * c->n_u_blocks * TU);
     c->d_counters = dalloc<unsigned int>(16);
     c->d_select = dalloc<SelectState>(1);
+    {  // small-N mode below kZqMaxSamples samples per shard (latency-bound sizes)
+      long long zq_max = kZqMaxSamples;
+      if (const char* e = getenv("SMPC_ZQ_MAX_SAMPLES")) zq_max = atoll(e);  // A/B knob (0 = off)
+      if (c->M_local <= zq_max) c->d_zq = dalloc<float4>((size_t)((TU + 3) / 4) * c->M_local);
+    }
     c->d_eq_cnt = dalloc<int>(c->n_w_blocks);
     c->d_eq_off = dalloc<long long>(c->n_w_blocks + 1);
     c->d_gather1 = dalloc<double>((size_t)c->S * 2 * 8);
@@ -855,7 +867,7 @@ void smpc_destroy(smpc_ctx* c) {
                   c->d_gather3, c->d_blk_arg, c->d_blk_nz, c->d_counters, c->d_costmap, c->d_result,
                   c->d_ro_x0, c->d_ro_mean, c->d_eps, c->d_outputs, c->d_wscratch, c->d_flags,
                   c->d_cand, c->d_cand_cnt, c->d_cand_off, c->d_select, c->d_eq_cnt, c->d_eq_off,
-                  c->d_dyn_tensor};
+                  c->d_dyn_tensor, c->d_zq};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->h_result) cudaFreeHost(c->h_result);
@@ -1327,8 +1339,10 @@ void* smpc_stream(smpc_ctx* c) { return c ? (void*)c->stream : nullptr; }
 
 int32_t smpc_kernels_per_solve(const smpc_ctx* c) {
   if (!c) return 0;
-  if (c->p.controller_kind == SMPC_CTRL_CEM) return 2 + c->I * (1 + 11 + 1);  // rollout, select (init+8+2), update
-  return 2 + c->I * (3 + (c->world > 1 ? 1 : 0));
+  const int zq = c->d_zq ? 1 : 0;  // gen_zq_kernel per iteration in small-N mode
+  const int rm = c->p.controller_kind == SMPC_CTRL_RMPPI ? 1 : 0;
+  if (c->p.controller_kind == SMPC_CTRL_CEM) return 2 + c->I * (1 + 11 + 1 + zq);  // rollout, select (init+8+2), update
+  return 2 + rm + c->I * (3 + zq + (c->world > 1 ? 1 : 0));
 }
 
 smpc_status smpc_icdf_domain(smpc_ctx* c, float* out) {
