@@ -25,7 +25,7 @@ EXPORTED = [
     "smpc_launch_iteration", "smpc_synchronize", "smpc_stream", "smpc_kernels_per_solve",
     "smpc_rollout_kernel_ms", "smpc_icdf_domain", "smpc_comm_unique_id", "smpc_comm_init", "smpc_group_init",
     "smpc_group_compute_control", "smpc_host_libm_uses_fma",
-    "smpc_measure_fp32_peak", "smpc_version",
+    "smpc_measure_fp32_peak", "smpc_sqrt_check", "smpc_version",
 ]
 
 _lib = None
@@ -103,6 +103,8 @@ def load(path: str = None) -> ctypes.CDLL:
     L.smpc_host_libm_uses_fma.restype = ctypes.c_int32
     L.smpc_measure_fp32_peak.argtypes = [ctypes.c_int32, P(ctypes.c_double)]
     L.smpc_measure_fp32_peak.restype = ctypes.c_int
+    L.smpc_sqrt_check.argtypes = [ctypes.c_int32, P(ctypes.c_uint64)]
+    L.smpc_sqrt_check.restype = ctypes.c_int
     L.smpc_version.argtypes = []
     L.smpc_version.restype = ctypes.c_char_p
     for name in ["smpc_create", "smpc_error_location", "smpc_get_dims", "smpc_set_mean", "smpc_get_mean",

@@ -124,8 +124,10 @@ struct IterArgs {
   uint32_t key0, key1;
   PhiloxKeys rk;         // round keys of (key0, key1)
   PackConst pk;
-  uint32_t j_lo, j_hi;   // uniform index j = w >> 9 is a lower tail iff j < j_lo, upper iff j >= j_hi
-  uint32_t tail_hi_base; // N + 2^23 - 1: upper-tail entry of j is tail[tail_hi_base - j]
+  // Phi^-1 tail lookup on the Philox word w (see philox_normal.cuh): with
+  // u = w + tail_off (mod 2^32), the draw is a tail iff u < tail_lim, and its
+  // value is tail[u >> 9] (upper tail first, then the lower tail).
+  uint32_t tail_off, tail_lim;
   int with_mean;
   long long zero_begin;
   int importance;
@@ -216,7 +218,7 @@ cudaError_t launch_select(const IterArgs& a, SelectState* st, long long k, unsig
                           long long* eq_off, cudaStream_t stream);
 cudaError_t launch_sort_selected(const IterArgs& a, long long k, unsigned long long* keys, long long* idx,
                                  unsigned long long* slot, cudaStream_t stream);
-cudaError_t build_tail_table(float* table, uint32_t n, cudaStream_t stream);
+cudaError_t build_tail_table(float* table, uint32_t j_lo, uint32_t j_hi, cudaStream_t stream);
 cudaError_t launch_begin_solve(ResultHeader* h, cudaStream_t stream);
 cudaError_t launch_shift_mean(float* mean, int S, int T, int NU, long long steps, cudaStream_t stream);
 cudaError_t launch_gen_zq(const IterArgs& a, int nu, float4* zq, cudaStream_t stream);

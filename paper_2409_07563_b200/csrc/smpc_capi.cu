@@ -356,7 +356,12 @@ void fill_args(smpc_ctx* c) {
   }
   a.pk.one = 0x3f8000003f800000ull;    // {1.0f, 1.0f}
   a.pk.mzero = 0x8000000080000000ull;  // {-0.0f, -0.0f}
-  a.tail_hi_base = tail_table_size(&a.j_lo, &a.j_hi) + (1u << 23) - 1u;
+  {
+    uint32_t j_lo, j_hi;
+    tail_table_size(&j_lo, &j_hi);
+    a.tail_off = ((1u << 23) - j_hi) << 9;           // rotates the upper tail to index 0
+    a.tail_lim = (((1u << 23) - j_hi) + j_lo) << 9;  // upper + lower tail entries
+  }
   a.with_mean = p.include_mean_sample != 0;
   // zero-mean quota filled from the tail (sampling.cpp:56-62)
   long long n_zero = (long long)ceil(p.zero_mean_fraction * (double)c->M);
@@ -832,9 +837,10 @@ smpc_status smpc_create(const smpc_problem* problem, smpc_ctx** out) {
       c->d_dyn_tensor = dalloc<float>(dyn_tensor.size());
       CK(cudaMemcpy(c->d_dyn_tensor, dyn_tensor.data(), sizeof(float) * dyn_tensor.size(), cudaMemcpyHostToDevice));
     }
-    const uint32_t n_tab = tail_table_size(nullptr, nullptr);
-    c->d_tail = dalloc<float>(2 * (size_t)n_tab);
-    CK(build_tail_table(c->d_tail, n_tab, c->stream));
+    uint32_t j_lo, j_hi;
+    tail_table_size(&j_lo, &j_hi);
+    c->d_tail = dalloc<float>((size_t)((1u << 23) - j_hi) + j_lo);
+    CK(build_tail_table(c->d_tail, j_lo, j_hi, c->stream));
     c->host_mean[0].assign(TU, 0.f);
     c->host_mean[1].assign(TU, 0.f);
     c->nominal_state.assign(c->nx, 0.f);

@@ -84,6 +84,16 @@ def test_icdf_whole_domain_bit_exact(mods):
     assert bad.size == 0, (bad[:10], out[bad[:10]], ref[bad[:10]])
 
 
+def test_branch_free_sqrt_exhaustive(mods):
+    """The cost / dynamics functors' branch-free sqrt (std::sqrt of
+    costs.cpp:59, the quaternion norm) equals sqrt.rn.f32 on all 2^32 floats."""
+    import ctypes
+    from paper_2409_07563_b200 import _lib
+    n = ctypes.c_uint64(123)
+    assert _lib.load().smpc_sqrt_check(0, ctypes.byref(n)) == 0
+    assert n.value == 0, n.value
+
+
 @pytest.mark.parametrize("name", ["cartpole", "double_integrator", "diff_drive_nav", "unicycle_road",
                                   "cartpole_road_perstep", "di_quadratic_dmd", "quadrotor", "bicycle_nav"])
 def test_generate_samples_bit_exact(mods, name):
