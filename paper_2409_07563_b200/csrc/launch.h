@@ -26,7 +26,7 @@ constexpr int kUpdateWarps = kUpdateThreads / 32;
 #ifndef SMPC_UPDATE_MIN_BLOCKS2
 #define SMPC_UPDATE_MIN_BLOCKS2 2
 #endif
-constexpr int kUpdateCtasPerSm = SMPC_UPDATE_MIN_BLOCKS2;  // resident update CTAs per SM (QPL = 2 bound)
+constexpr int kUpdateCtasPerSm = SMPC_UPDATE_MIN_BLOCKS2;  // resident update CTAs per SM
 // Shards up to this many samples pre-generate the iteration's noise in one
 // parallel pass (gen_zq_kernel) instead of inside each sample's serial chain.
 constexpr long long kZqMaxSamples = 16384;
@@ -161,10 +161,12 @@ struct IterArgs {
   long long* blk_nz;     // [S][n_w_blocks]
   double* gather2;       // [world][S][2]  (eta_g, nonzero_g)
   int* cand;             // [S][M_local] update candidates, compacted per weights-CTA range
+  double* cand_e;        // [S][M_local] e_m of each candidate (same positions as cand), or nullptr
   int* cand_cnt;         // [S][n_w_blocks]
   long long* cand_off;   // [S][n_w_blocks + 1] exclusive prefix of cand_cnt
   int n_u_blocks;
-  double* blk_part;      // [S][n_u_blocks][T*NU]
+  double* blk_part;      // [S][n_u_blocks * kUpdateWarps][upd_slots][4] per-warp quad sums
+  int upd_slots;         // q-runs one update warp can close: ceil(Q / warps) + 3
   double* gather3;       // [world][S][T*NU]
   // results
   ResultHeader* header;

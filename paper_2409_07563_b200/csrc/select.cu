@@ -147,7 +147,11 @@ __global__ void __launch_bounds__(256) select_mark_kernel(const IterArgs a, cons
       before += (w < warp) ? warp_cnt[w] : 0;
       total += warp_cnt[w];
     }
-    if (take) a.cand[beg + ncand + before + __popc(bal & ((1u << lane) - 1u))] = (int)i;
+    if (take) {
+      const long long pos = beg + ncand + before + __popc(bal & ((1u << lane) - 1u));
+      a.cand[pos] = (int)i;
+      if (a.cand_e) a.cand_e[pos] = 1.0;  // elites: e_m = 1, eta = 1
+    }
     ncand += total;
     __syncthreads();
   }

@@ -114,6 +114,8 @@ struct smpc_ctx {
   double *d_blk_min = nullptr, *d_blk_eta = nullptr, *d_blk_part = nullptr;
   double *d_gather1 = nullptr, *d_gather2 = nullptr, *d_gather3 = nullptr;
   int *d_cand = nullptr, *d_cand_cnt = nullptr;
+  double* d_cand_e = nullptr;
+  int upd_slots = 4;
   long long* d_cand_off = nullptr;
   long long *d_blk_arg = nullptr, *d_blk_nz = nullptr;
   unsigned int* d_counters = nullptr;
@@ -403,6 +405,8 @@ void fill_args(smpc_ctx* c) {
   a.blk_nz = c->d_blk_nz;
   a.gather2 = c->d_gather2;
   a.cand = c->d_cand;
+  a.cand_e = c->d_cand_e;
+  a.upd_slots = c->upd_slots;
   a.cand_cnt = c->d_cand_cnt;
   a.cand_off = c->d_cand_off;
   a.n_u_blocks = c->n_u_blocks;
@@ -775,7 +779,13 @@ smpc_status smpc_create(const smpc_problem* problem, smpc_ctx** out) {
     c->d_cand = dalloc<int>((size_t)c->S * c->M_local);
     c->d_cand_cnt = dalloc<int>((size_t)c->S * c->n_w_blocks);
     c->d_cand_off = dalloc<long long>((size_t)c->S * (c->n_w_blocks + 1));
-    c->d_blk_part = dalloc<double>((size_t)c->S * c->n_u_blocks * TU);
+    c->d_cand_e = dalloc<double>((size_t)c->S * c->M_local);
+    {
+      const long long warps = (long long)c->n_u_blocks * kUpdateWarps;
+      const long long Q = (TU + 3) / 4;
+      c->upd_slots = (int)((Q + warps - 1) / warps + 3);
+      c->d_blk_part = dalloc<double>((size_t)c->S * warps * c->upd_slots * 4);
+    }
     c->d_counters = dalloc<unsigned int>(16);
     c->d_select = dalloc<SelectState>(1);
     {  // small-N mode below kZqMaxSamples samples per shard (latency-bound sizes)
@@ -872,7 +882,7 @@ void smpc_destroy(smpc_ctx* c) {
                   c->d_weights, c->d_blk_min, c->d_blk_eta, c->d_blk_part, c->d_gather1, c->d_gather2,
                   c->d_gather3, c->d_blk_arg, c->d_blk_nz, c->d_counters, c->d_costmap, c->d_result,
                   c->d_ro_x0, c->d_ro_mean, c->d_eps, c->d_outputs, c->d_wscratch, c->d_flags,
-                  c->d_cand, c->d_cand_cnt, c->d_cand_off, c->d_select, c->d_eq_cnt, c->d_eq_off,
+                  c->d_cand, c->d_cand_e, c->d_cand_cnt, c->d_cand_off, c->d_select, c->d_eq_cnt, c->d_eq_off,
                   c->d_dyn_tensor, c->d_zq};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -1189,6 +1199,7 @@ smpc_status smpc_compute_weights(smpc_ctx* c, const double* costs, int64_t count
     a.blk_eta = d_eta;
     a.blk_nz = reinterpret_cast<long long*>(d_nz);
     a.cand = d_cand;
+    a.cand_e = nullptr;  // weights only: no update follows
     a.cand_cnt = d_ccnt;
     a.cand_off = d_coff;
     CK(launch_weights(a, c->stream));
