@@ -165,8 +165,8 @@ struct IterArgs {
   int* cand_cnt;         // [S][n_w_blocks]
   long long* cand_off;   // [S][n_w_blocks + 1] exclusive prefix of cand_cnt
   int n_u_blocks;
-  double* blk_part;      // [S][n_u_blocks * kUpdateWarps][upd_slots][4] per-warp quad sums
-  int upd_slots;         // q-runs one update warp can close: ceil(Q / warps) + 3
+  double* blk_part;      // [S][Q][upd_slots][4] per-warp quad sums, by rank among the quad's warps
+  int upd_slots;         // max warps covering one quad
   double* gather3;       // [world][S][T*NU]
   // results
   ResultHeader* header;

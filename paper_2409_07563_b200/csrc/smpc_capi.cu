@@ -783,8 +783,9 @@ smpc_status smpc_create(const smpc_problem* problem, smpc_ctx** out) {
     {
       const long long warps = (long long)c->n_u_blocks * kUpdateWarps;
       const long long Q = (TU + 3) / 4;
-      c->upd_slots = (int)((Q + warps - 1) / warps + 3);
-      c->d_blk_part = dalloc<double>((size_t)c->S * warps * c->upd_slots * 4);
+      // warps covering one quad: <= 2 * warps / Q + 2 (each owns >= U / (2 W) units)
+      c->upd_slots = (int)(2 * ((warps + Q - 1) / Q) + 3);
+      c->d_blk_part = dalloc<double>((size_t)c->S * Q * c->upd_slots * 4);
     }
     c->d_counters = dalloc<unsigned int>(16);
     c->d_select = dalloc<SelectState>(1);
