@@ -131,6 +131,38 @@ def test_rollout_costs_bit_exact(mods, name, systems):
     assert np.array_equal(o_gen.view(np.uint32), o_ref.view(np.uint32))
 
 
+@pytest.mark.parametrize("name", ["cartpole", "double_integrator", "diff_drive_nav", "unicycle_road",
+                                  "cartpole_road_perstep", "di_quadratic_dmd", "quadrotor", "bicycle_nav",
+                                  "di_circle_at_rest"])
+@pytest.mark.parametrize("systems", [1, 2])
+def test_rollout_costs_fast_path_bit_exact(mods, name, systems):
+    """The unchecked fast loop (no stored outputs: sticky flags, fast sqrt,
+    branch-free two-quad steady state) gives the oracle's costs bit for bit.
+    di_circle_at_rest: zero velocity and zero mean, so the mean sample's
+    speed is exactly 0 every step (sqrt edge case -> exact replay)."""
+    S = mods["S"]
+    if name == "di_circle_at_rest":
+        sc = S.Scenario(num_samples=777, horizon=50, dt=0.02, lambda_=1.0, control_std=(1.0, 1.0), rng_seed=5,
+                        importance_sampling=False, dynamics="double_integrator", cost="circle_track",
+                        initial_state={"X": 2.0})
+    else:
+        sc = scenarios(S)[name]
+    n_x, n_u, n_y = sc.dims
+    T = sc.horizon
+    rng = np.random.default_rng(2)
+    means = (rng.standard_normal((systems, T, n_u)) * 0.2).astype(np.float32)
+    if name == "di_circle_at_rest":
+        means[:] = 0.0
+    x0s = np.stack([sc.x0() + (0.05 * s if name != "di_circle_at_rest" else 0.0) for s in range(systems)])
+    x0s = x0s.astype(np.float32)
+    eng = mods["C"].RolloutEngine(sc)
+    O = mods["Oracle"]("port")
+    eps, _ = O.generate_samples(sc, means[0], 17)
+    c_ref, _ = O.rollout(sc, x0s, means, eps, outputs=True)
+    c_gen = eng.rollout(x0s, means, stream=17)
+    assert np.array_equal(c_gen.view(np.uint64), c_ref.view(np.uint64))
+
+
 def test_compute_weights_matches_oracle(mods):
     rng = np.random.default_rng(1)
     eng = mods["C"].RolloutEngine(mods["S"].cartpole_scenario(num_samples=64, horizon=10))
