@@ -146,6 +146,7 @@ struct IterArgs {
   const double* gamma;   // [T]
   const float* eps_in;   // injected [M_local][T][NU] or nullptr
   const float* tail;     // Phi^-1 tail table
+  unsigned long long tail_tex;  // the same table as a 1-D texture object (index-addressed fetch)
   // rollout outputs
   double* costs;   // [S][M_local]
   float* outputs;  // [S][M_local][T][NY] or nullptr

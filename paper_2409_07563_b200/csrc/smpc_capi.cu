@@ -115,6 +115,7 @@ struct smpc_ctx {
   double *d_gather1 = nullptr, *d_gather2 = nullptr, *d_gather3 = nullptr;
   int *d_cand = nullptr, *d_cand_cnt = nullptr;
   double* d_cand_e = nullptr;
+  unsigned long long tail_tex = 0;
   int upd_slots = 4;
   long long* d_cand_off = nullptr;
   long long *d_blk_arg = nullptr, *d_blk_nz = nullptr;
@@ -392,6 +393,7 @@ void fill_args(smpc_ctx* c) {
   a.sample_idx = nullptr;
   a.zq = nullptr;
   a.tail = c->d_tail;
+  a.tail_tex = c->tail_tex;
   a.costs = c->d_costs;
   a.outputs = nullptr;
   a.n_roll_blocks = c->n_roll_blocks;
@@ -852,6 +854,18 @@ smpc_status smpc_create(const smpc_problem* problem, smpc_ctx** out) {
     tail_table_size(&j_lo, &j_hi);
     c->d_tail = dalloc<float>((size_t)((1u << 23) - j_hi) + j_lo);
     CK(build_tail_table(c->d_tail, j_lo, j_hi, c->stream));
+    {
+      cudaResourceDesc rd = {};
+      rd.resType = cudaResourceTypeLinear;
+      rd.res.linear.devPtr = c->d_tail;
+      rd.res.linear.desc = cudaCreateChannelDesc<float>();
+      rd.res.linear.sizeInBytes = sizeof(float) * ((size_t)((1u << 23) - j_hi) + j_lo);
+      cudaTextureDesc td = {};
+      td.readMode = cudaReadModeElementType;
+      cudaTextureObject_t tex = 0;
+      CK(cudaCreateTextureObject(&tex, &rd, &td, nullptr));
+      c->tail_tex = (unsigned long long)tex;
+    }
     c->host_mean[0].assign(TU, 0.f);
     c->host_mean[1].assign(TU, 0.f);
     c->nominal_state.assign(c->nx, 0.f);
@@ -876,6 +890,7 @@ void smpc_destroy(smpc_ctx* c) {
   if (!c) return;
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->graph) cudaGraphExecDestroy(c->graph);
+  if (c->tail_tex) cudaDestroyTextureObject((cudaTextureObject_t)c->tail_tex);
   for (auto e : c->ev) cudaEventDestroy(e);
   if (c->ev_stage) cudaEventDestroy(c->ev_stage);
   if (c->comm && nccl()) nccl()->CommDestroy(c->comm);
