@@ -25,7 +25,8 @@ EXPORTED = [
     "smpc_launch_iteration", "smpc_synchronize", "smpc_stream", "smpc_kernels_per_solve",
     "smpc_rollout_kernel_ms", "smpc_icdf_domain", "smpc_comm_unique_id", "smpc_comm_init", "smpc_group_init",
     "smpc_group_compute_control", "smpc_host_libm_uses_fma",
-    "smpc_measure_fp32_peak", "smpc_sqrt_check", "smpc_version",
+    "smpc_measure_fp32_peak", "smpc_sqrt_check", "smpc_select_noise_strategy", "smpc_noise_strategy_rule",
+    "smpc_version",
 ]
 
 _lib = None
@@ -42,6 +43,15 @@ class SmpcError(RuntimeError):
 
 class SmpcConfigError(SmpcError):
     """smpc::ConfigError."""
+
+
+NOISE_AUTO, NOISE_SPLIT, NOISE_FUSED = 0, 1, 2
+
+
+class SmpcNoiseChoice(ctypes.Structure):
+    """smpc_noise_choice (include/smpc_b200.h)."""
+    _fields_ = [("kind", ctypes.c_int32), ("split_median_ms", ctypes.c_double),
+                ("fused_median_ms", ctypes.c_double), ("timed", ctypes.c_int32)]
 
 
 def load(path: str = None) -> ctypes.CDLL:
@@ -105,6 +115,11 @@ def load(path: str = None) -> ctypes.CDLL:
     L.smpc_measure_fp32_peak.restype = ctypes.c_int
     L.smpc_sqrt_check.argtypes = [ctypes.c_int32, P(ctypes.c_uint64)]
     L.smpc_sqrt_check.restype = ctypes.c_int
+    L.smpc_select_noise_strategy.argtypes = [c_ctx, ctypes.c_int32, ctypes.c_int32, ctypes.c_double, f32p,
+                                             P(SmpcNoiseChoice)]
+    L.smpc_select_noise_strategy.restype = ctypes.c_int
+    L.smpc_noise_strategy_rule.argtypes = [ctypes.c_double] * 4
+    L.smpc_noise_strategy_rule.restype = ctypes.c_int32
     L.smpc_version.argtypes = []
     L.smpc_version.restype = ctypes.c_char_p
     for name in ["smpc_create", "smpc_error_location", "smpc_get_dims", "smpc_set_mean", "smpc_get_mean",

@@ -130,6 +130,25 @@ class RolloutEngine(_Context):
             float(fraction), ctypes.byref(k), order.ctypes.data, outs.ctypes.data))
         return order[:k.value], outs[:k.value * self.T * self.n_y].reshape(k.value, self.T, self.n_y)
 
+    def select_noise_strategy(self, kind: str = "auto", trials: int = 0, split_budget_bytes: float = 256 << 20,
+                              x0=None) -> dict:
+        """RolloutEngine::auto_select / set_strategy (engine.cpp:281-335) for the
+        device's noise evaluation orders: "split" (normals materialised by one
+        parallel pass) or "fused" (regenerated in registers); "auto" applies
+        the scratch budget, then times both from x0 (median of max(3, trials)
+        after 2 warm-ups) and keeps fused only if strictly faster."""
+        from ._lib import SmpcNoiseChoice, NOISE_AUTO, NOISE_SPLIT, NOISE_FUSED
+        k = {"auto": NOISE_AUTO, "split": NOISE_SPLIT, "fused": NOISE_FUSED}[kind]
+        ch = SmpcNoiseChoice()
+        x = _f32(x0 if x0 is not None else self.scenario.x0()).ravel()
+        if x.size == self.n_x:  # the same state for both systems of a Tube controller
+            x = np.tile(x, 2)
+        self._check(self.lib.smpc_select_noise_strategy(self.ctx, k, int(trials), float(split_budget_bytes), x,
+                                                        ctypes.byref(ch)))
+        return {"kind": {NOISE_SPLIT: "split", NOISE_FUSED: "fused"}[ch.kind],
+                "split_median_ms": ch.split_median_ms, "fused_median_ms": ch.fused_median_ms,
+                "timed": bool(ch.timed)}
+
     def compute_weights(self, costs, lam: float) -> WeightResult:
         costs = np.ascontiguousarray(costs, np.float64).ravel()
         w = np.zeros_like(costs)

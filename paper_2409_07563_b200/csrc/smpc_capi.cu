@@ -123,6 +123,9 @@ struct smpc_ctx {
   uint8_t* d_costmap = nullptr;
   float* d_dyn_tensor = nullptr;
   float4* d_zq = nullptr;  // small-N mode noise buffer [Q][M_local]
+  bool use_zq = false;     // noise strategy: split (d_zq pass) vs fused (in-register)
+  smpc_noise_choice noise_choice = {SMPC_NOISE_AUTO, 0.0, 0.0, 0};
+  bool noise_resolved = false;  // set by smpc_select_noise_strategy (default: split iff M_local <= 16384)
   // CEM elite selection / sample ordering (select.cu)
   SelectState* d_select = nullptr;
   int* d_eq_cnt = nullptr;
@@ -543,7 +546,7 @@ void enqueue_solve(smpc_ctx* c, bool timed) {
     a.iter = it;
     a.do_finish = it == c->I - 1;
     if (timed) CK(cudaEventRecord(c->ev[2 * it], c->stream));
-    if (c->d_zq) {  // small-N mode: the noise as one parallel pass, off the per-sample serial chain
+    if (c->use_zq) {  // split noise: one parallel pass, off the per-sample serial chain
       a.zq = c->d_zq;
       CK(launch_gen_zq(a, c->nu, c->d_zq, c->stream));
     }
@@ -643,6 +646,85 @@ void build_graph(smpc_ctx* c) {
   CK(cudaStreamEndCapture(c->stream, &g));
   CK(cudaGraphInstantiate(&c->graph, g, 0));
   cudaGraphDestroy(g);
+}
+
+void set_noise(smpc_ctx* c, bool split) {
+  if (split && !c->d_zq) c->d_zq = dalloc<float4>((size_t)((c->T * c->nu + 3) / 4) * c->M_local);
+  if (c->use_zq != split) {
+    c->use_zq = split;
+    if (c->graph) {
+      cudaGraphExecDestroy(c->graph);
+      c->graph = nullptr;
+    }
+  }
+}
+
+// One iteration (noise, rollout, weights / elite selection, weighted
+// update) of the current means from d_x0, with the update committed into a
+// scratch mean: the controller state is untouched. Unlike the reference's
+// CPU strategies, the device ones also differ in the update (split reads the
+// materialised normals back), so the whole iteration is what is timed.
+double time_iteration_median(smpc_ctx* c, bool split, int n) {
+  IterArgs a = c->base;
+  a.do_finish = 0;
+  a.iter = 0;
+  if (split) a.zq = c->d_zq;
+  float* scratch = nullptr;
+  CK(cudaMalloc(&scratch, sizeof(float) * (size_t)c->S * c->T * c->nu));
+  a.mean_out = scratch;
+  auto once = [&] {
+    CK(launch_begin_solve(c->header(), c->stream));
+    if (split) CK(launch_gen_zq(a, c->nu, c->d_zq, c->stream));
+    CK(c->ops.rollout(a, c->p.cost_kind, c->stream));
+    if (c->world > 1) return;  // the rest needs the collectives: rollout only
+    if (c->p.controller_kind == SMPC_CTRL_CEM) {
+      CK(launch_select(a, c->d_select, c->cem_k, c->d_counters + 8, c->d_eq_cnt, c->d_eq_off, c->stream));
+    } else {
+      CK(c->ops.weights(a, c->stream));
+    }
+    CK(c->ops.update(a, c->stream));
+  };
+  std::vector<double> t;
+  try {
+    for (int i = 0; i < 2; ++i) once();
+    for (int i = 0; i < n; ++i) {
+      CK(cudaEventRecord(c->ev[0], c->stream));
+      once();
+      CK(cudaEventRecord(c->ev[1], c->stream));
+      CK(cudaEventSynchronize(c->ev[1]));
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
+      t.push_back(ms);
+    }
+  } catch (...) {
+    cudaStreamSynchronize(c->stream);
+    cudaFree(scratch);
+    throw;
+  }
+  CK(cudaStreamSynchronize(c->stream));
+  cudaFree(scratch);
+  std::sort(t.begin(), t.end());
+  return t.size() % 2 ? t[t.size() / 2] : 0.5 * (t[t.size() / 2 - 1] + t[t.size() / 2]);
+}
+
+// The AUTO selection from the states already in d_x0.
+smpc_noise_choice auto_select_noise(smpc_ctx* c, int32_t trials, double split_budget_bytes) {
+  smpc_noise_choice ch = {SMPC_NOISE_AUTO, 0.0, 0.0, 0};
+  const double split_bytes = 16.0 * (double)((c->T * c->nu + 3) / 4) * (double)c->M_local;
+  if (split_bytes > split_budget_bytes) {
+    ch.kind = SMPC_NOISE_FUSED;
+  } else {
+    const int n = std::max(3, trials > 0 ? trials : 5);
+    set_noise(c, true);
+    ch.split_median_ms = time_iteration_median(c, true, n);
+    ch.fused_median_ms = time_iteration_median(c, false, n);
+    ch.timed = 1;
+    ch.kind = smpc_noise_strategy_rule(split_bytes, split_budget_bytes, ch.split_median_ms, ch.fused_median_ms);
+  }
+  set_noise(c, ch.kind == SMPC_NOISE_SPLIT);
+  c->noise_choice = ch;
+  c->noise_resolved = true;
+  return ch;
 }
 
 void launch_solve(smpc_ctx* c) {
@@ -794,7 +876,10 @@ smpc_status smpc_create(const smpc_problem* problem, smpc_ctx** out) {
     {  // small-N mode below kZqMaxSamples samples per shard (latency-bound sizes)
       long long zq_max = kZqMaxSamples;
       if (const char* e = getenv("SMPC_ZQ_MAX_SAMPLES")) zq_max = atoll(e);  // A/B knob (0 = off)
-      if (c->M_local <= zq_max) c->d_zq = dalloc<float4>((size_t)((TU + 3) / 4) * c->M_local);
+      if (c->M_local <= zq_max) {
+        c->d_zq = dalloc<float4>((size_t)((TU + 3) / 4) * c->M_local);
+        c->use_zq = true;
+      }
     }
     c->d_eq_cnt = dalloc<int>(c->n_w_blocks);
     c->d_eq_off = dalloc<long long>(c->n_w_blocks + 1);
@@ -1340,6 +1425,36 @@ smpc_status smpc_export_sample_trajectories(smpc_ctx* c, const float* x0, const 
   });
 }
 
+// RolloutEngine::auto_select (engine.cpp:281-320) for the device's two noise
+// strategies (split = materialised normals, fused = in-register Philox): a
+// scratch budget first, then medians of timed runs, fused only if strictly
+// faster (ties -> split).
+extern "C" int32_t smpc_noise_strategy_rule(double split_bytes, double split_budget_bytes, double split_median_ms,
+                                            double fused_median_ms) {
+  if (split_bytes > split_budget_bytes) return SMPC_NOISE_FUSED;
+  return fused_median_ms < split_median_ms ? SMPC_NOISE_FUSED : SMPC_NOISE_SPLIT;
+}
+
+
+smpc_status smpc_select_noise_strategy(smpc_ctx* c, int32_t kind, int32_t trials, double split_budget_bytes,
+                                       const float* x0, smpc_noise_choice* out) {
+  if (!c || kind < SMPC_NOISE_AUTO || kind > SMPC_NOISE_FUSED || (kind == SMPC_NOISE_AUTO && !x0))
+    return SMPC_ERR_ARGUMENT;
+  return guarded(c, [&] {
+    smpc_noise_choice ch = {kind, 0.0, 0.0, 0};
+    if (kind == SMPC_NOISE_AUTO) {
+      upload_x0(c, x0, c->S);
+      ch = auto_select_noise(c, trials, split_budget_bytes);
+    } else {
+      set_noise(c, kind == SMPC_NOISE_SPLIT);
+      c->noise_choice = ch;
+      c->noise_resolved = true;
+    }
+    if (out) *out = ch;
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
 smpc_status smpc_set_x0(smpc_ctx* c, const float* x0) {
   if (!c || !x0) return SMPC_ERR_ARGUMENT;
   return guarded(c, [&] {
@@ -1372,7 +1487,7 @@ void* smpc_stream(smpc_ctx* c) { return c ? (void*)c->stream : nullptr; }
 
 int32_t smpc_kernels_per_solve(const smpc_ctx* c) {
   if (!c) return 0;
-  const int zq = c->d_zq ? 1 : 0;  // gen_zq_kernel per iteration in small-N mode
+  const int zq = c->use_zq ? 1 : 0;  // gen_zq_kernel per iteration in split-noise mode
   const int rm = c->p.controller_kind == SMPC_CTRL_RMPPI ? 1 : 0;
   if (c->p.controller_kind == SMPC_CTRL_CEM) return 2 + c->I * (1 + 11 + 1 + zq);  // rollout, select (init+8+2), update
   return 2 + rm + c->I * (3 + zq + (c->world > 1 ? 1 : 0));

@@ -76,3 +76,18 @@ def test_config_errors_need_no_gpu(lib):
     with pytest.raises(SmpcError, match=r"^mppi: iterations must be in \[1, 256\]$"):
         make_controller(S.Scenario(num_samples=16, horizon=5, dynamics="cartpole", cost="road", control_std=(1.0,),
                                    iterations=300))
+
+
+def test_noise_strategy_rule_mirrors_auto_select():
+    """RolloutEngine::auto_select's decision (engine.cpp:281-320; tested with
+    an injected clock in test_engine.cpp:334-390): over the scratch budget ->
+    the no-scratch strategy; otherwise fused only if strictly faster, ties ->
+    split. Pure function, no GPU needed."""
+    from paper_2409_07563_b200 import _lib
+    L = _lib.load()
+    SPLIT, FUSED = _lib.NOISE_SPLIT, _lib.NOISE_FUSED
+    assert L.smpc_noise_strategy_rule(1e9, 1e6, 1.0, 5.0) == FUSED   # budget exceeded: no timing matters
+    assert L.smpc_noise_strategy_rule(1e3, 1e6, 2.0, 1.0) == FUSED   # fused strictly faster
+    assert L.smpc_noise_strategy_rule(1e3, 1e6, 1.0, 2.0) == SPLIT
+    assert L.smpc_noise_strategy_rule(1e3, 1e6, 1.5, 1.5) == SPLIT   # tie -> split
+    assert L.smpc_noise_strategy_rule(1e6, 1e6, 1.0, 2.0) == SPLIT   # at the budget is within it

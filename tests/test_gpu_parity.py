@@ -328,3 +328,34 @@ def test_shard_group_matches_single(mods, name, n):
         assert close(a.states, b["states"])
         for m in grp.members:
             m.set_mean(b["controls"])
+
+
+@pytest.mark.parametrize("name", ["cartpole", "double_integrator", "quadrotor"])
+def test_noise_strategies_bit_identical(mods, name):
+    """split (materialised normals) and fused (in-register) noise give the
+    same solves bit for bit (the reference's split == fused contract,
+    test_engine.cpp:86-99); auto times both and follows the decision rule."""
+    from paper_2409_07563_b200 import _lib
+    sc = scenarios(mods["S"])[name]
+    a = mods["C"].make_controller(sc)
+    b = mods["C"].make_controller(sc)
+    assert a.select_noise_strategy("split")["kind"] == "split"
+    assert b.select_noise_strategy("fused")["kind"] == "fused"
+    x = sc.x0()
+    for _ in range(3):
+        sa, sb = a.compute_control(x), b.compute_control(x)
+        assert sa.weights.baseline == sb.weights.baseline and sa.weights.argmin == sb.weights.argmin
+        assert np.array_equal(sa.controls.view(np.uint32), sb.controls.view(np.uint32))
+        assert np.array_equal(sa.states.view(np.uint32), sb.states.view(np.uint32))
+    ch = a.select_noise_strategy("auto", trials=3)
+    assert ch["timed"] and ch["split_median_ms"] > 0 and ch["fused_median_ms"] > 0
+    rule = _lib.load().smpc_noise_strategy_rule(0.0, 1.0, ch["split_median_ms"], ch["fused_median_ms"])
+    assert ch["kind"] == {_lib.NOISE_SPLIT: "split", _lib.NOISE_FUSED: "fused"}[rule]
+    # auto must not disturb the controller: the next solve continues the sequence
+    sa, sb = a.compute_control(x), b.compute_control(x)
+    assert np.array_equal(sa.controls.view(np.uint32), sb.controls.view(np.uint32))
+    # over the scratch budget -> fused without timing
+    ch = a.select_noise_strategy("auto", split_budget_bytes=0.0)
+    assert ch["kind"] == "fused" and not ch["timed"]
+    a.close()
+    b.close()
