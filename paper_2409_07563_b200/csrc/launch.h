@@ -27,6 +27,10 @@ constexpr int kUpdateWarps = kUpdateThreads / 32;
 #define SMPC_UPDATE_MIN_BLOCKS2 2
 #endif
 constexpr int kUpdateCtasPerSm = SMPC_UPDATE_MIN_BLOCKS2;  // resident update CTAs per SM
+#ifndef SMPC_UPDATE_QUADS_PER_UNIT
+#define SMPC_UPDATE_QUADS_PER_UNIT 2
+#endif
+constexpr int kUpdateQuadsPerUnit = SMPC_UPDATE_QUADS_PER_UNIT;  // quads per update work unit
 // Shards up to this many samples pre-generate the iteration's noise in one
 // parallel pass (gen_zq_kernel) instead of inside each sample's serial chain.
 constexpr long long kZqMaxSamples = 16384;
@@ -166,8 +170,8 @@ struct IterArgs {
   int* cand_cnt;         // [S][n_w_blocks]
   long long* cand_off;   // [S][n_w_blocks + 1] exclusive prefix of cand_cnt
   int n_u_blocks;
-  double* blk_part;      // [S][Q][upd_slots][4] per-warp quad sums, by rank among the quad's warps
-  int upd_slots;         // max warps covering one quad
+  double* blk_part;      // [S][QG][upd_slots][QW][4] per-warp quad sums, by rank among the group's warps
+  int upd_slots;         // max warps covering one quad group
   double* gather3;       // [world][S][T*NU]
   // results
   ResultHeader* header;

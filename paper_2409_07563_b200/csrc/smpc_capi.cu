@@ -866,10 +866,10 @@ smpc_status smpc_create(const smpc_problem* problem, smpc_ctx** out) {
     c->d_cand_e = dalloc<double>((size_t)c->S * c->M_local);
     {
       const long long warps = (long long)c->n_u_blocks * kUpdateWarps;
-      const long long Q = (TU + 3) / 4;
-      // warps covering one quad: <= 2 * warps / Q + 2 (each owns >= U / (2 W) units)
-      c->upd_slots = (int)(2 * ((warps + Q - 1) / Q) + 3);
-      c->d_blk_part = dalloc<double>((size_t)c->S * Q * c->upd_slots * 4);
+      const long long Q = (TU + 3) / 4, QG = (Q + kUpdateQuadsPerUnit - 1) / kUpdateQuadsPerUnit;
+      // warps covering one quad group: <= 2 * warps / QG + 2 (each owns >= U / (2 W) units)
+      c->upd_slots = (int)(2 * ((warps + QG - 1) / QG) + 3);
+      c->d_blk_part = dalloc<double>((size_t)c->S * QG * c->upd_slots * kUpdateQuadsPerUnit * 4);
     }
     c->d_counters = dalloc<unsigned int>(16);
     c->d_select = dalloc<SelectState>(1);
