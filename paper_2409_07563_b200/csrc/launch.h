@@ -4,6 +4,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <math.h>
 #include <stdint.h>
 
 namespace smpc_dev {
@@ -117,6 +118,15 @@ struct PlantStepArgs {
   double* log;            // [steps][2 + NX + NU] rows {t, x, u, c} or nullptr
 };
 
+__host__ __device__ inline double exact_inverse_pow2(double x) {
+  // 1/x if x is a power of two whose inverse is a normal double (then x*inv
+  // equals x/lambda bit for bit for every operand), else 0
+  if (!(x > 0.0) || x > 0x1p1000 || x < 0x1p-1000) return 0.0;
+  int e;
+  const double m = frexp(x, &e);
+  return m == 0.5 ? ldexp(1.0, 1 - e) : 0.0;
+}
+
 struct IterArgs {
   // problem
   int T, S;
@@ -125,6 +135,7 @@ struct IterArgs {
   long long M_global;
   float dt;
   double lambda;
+  double inv_lambda_pow2;  // 1/lambda when lambda is a power of two (x/lambda == x*inv exactly), else 0
   uint32_t key0, key1;
   PhiloxKeys rk;         // round keys of (key0, key1)
   PackConst pk;

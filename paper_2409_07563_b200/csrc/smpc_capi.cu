@@ -354,6 +354,7 @@ void fill_args(smpc_ctx* c) {
   a.M_global = c->M;
   a.dt = (float)p.dt;  // engine.cpp:136, :216
   a.lambda = p.lambda;
+  a.inv_lambda_pow2 = exact_inverse_pow2(p.lambda);
   a.key0 = (uint32_t)p.seed;
   a.key1 = (uint32_t)(p.seed >> 32);
   for (int r = 0; r < 10; ++r) {  // Philox round keys (rng.hpp:24-25)
@@ -1294,6 +1295,7 @@ smpc_status smpc_compute_weights(smpc_ctx* c, const double* costs, int64_t count
     a.costs = d_costs;
     a.weights = d_w;
     a.lambda = lambda;
+    a.inv_lambda_pow2 = exact_inverse_pow2(lambda);
     a.gather1 = d_g1;
     a.gather2 = d_g2;
     a.n_w_blocks = nblk;
