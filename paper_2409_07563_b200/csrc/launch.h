@@ -136,6 +136,7 @@ struct IterArgs {
   float dt;
   double lambda;
   double inv_lambda_pow2;  // 1/lambda when lambda is a power of two (x/lambda == x*inv exactly), else 0
+  int sig2_pow2;           // every sigma^2 is a power of two: the importance term multiplies by 1/sigma^2 (exact)
   uint32_t key0, key1;
   PhiloxKeys rk;         // round keys of (key0, key1)
   PackConst pk;

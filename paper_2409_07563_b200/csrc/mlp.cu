@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(kTile, 4) mlp_rollout_kernel(const IterArgs a,
   for (int e = tid; e < OUT; e += kTile) prm[HID * IN + 2 * HID + OUT * HID + e] = __ldg(w + B3 + e);
   for (int k = tid; k < TU; k += kTile) {
     sigma_s[k] = a.sigma[k];
-    if (IMP) sig2_s[k] = a.sig2[k];
+    if (IMP) sig2_s[k] = a.sig2_pow2 ? 1.0 / a.sig2[k] : a.sig2[k];  // exact inverse of a power of two
   }
   for (int k = tid; k < S * TU; k += kTile) mean_s[k] = a.mean_in[k];
   if (warp == 0) {
@@ -245,7 +245,10 @@ __global__ void __launch_bounds__(kTile, 4) mlp_rollout_kernel(const IterArgs a,
       }
       const float mu = mean_sys[k];
       u[c] = F_ADD(mu, e);
-      if constexpr (IMP) imp = D_ADD(imp, __ddiv_rn(D_MUL((double)mu, (double)e), sig2_s[k]));
+      if constexpr (IMP) {
+        const double me = D_MUL((double)mu, (double)e);
+        imp = D_ADD(imp, a.sig2_pow2 ? D_MUL(me, sig2_s[k]) : __ddiv_rn(me, sig2_s[k]));
+      }
     }
     dyn.clamp_control(u, uc);
     // ---- layer 1 (SIMT) -> this sample's row of the hi/lo A operand

@@ -921,6 +921,11 @@ smpc_status smpc_create(const smpc_problem* problem, smpc_ctx** out) {
       gam[t] = c->step_sizes.empty() ? 1.0 : (double)c->step_sizes[c->step_sizes.size() == 1 ? 0 : t];
     CK(cudaMemcpy(c->d_sigma, sig.data(), sizeof(float) * TU, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(c->d_sig2, sig2.data(), sizeof(double) * TU, cudaMemcpyHostToDevice));
+    {
+      bool pow2 = true;
+      for (double v : sig2) pow2 = pow2 && exact_inverse_pow2(v) != 0.0;
+      c->base.sig2_pow2 = pow2 ? 1 : 0;  // fill_args leaves it alone
+    }
     CK(cudaMemcpy(c->d_gamma, gam.data(), sizeof(double) * c->T, cudaMemcpyHostToDevice));
     if (p.cost_kind == SMPC_COST_DIFF_DRIVE_NAV) {
       const size_t cells = (size_t)p.costmap_cells_x * p.costmap_cells_y;
