@@ -3,6 +3,6 @@
 #include "inst_common.cuh"
 
 namespace smpc_dev {
-SMPC_DEFINE_OPS(bc_fma, BicycleDyn<true>, BicycleDyn<true> b; b.wheelbase = p.p[0]; b.lo[0] = p.p[1], b.hi[0] = p.p[2]; b.lo[1] = p.p[3], b.hi[1] = p.p[4]; return b;)
+SMPC_DEFINE_OPS(bc_fma, BicycleDyn<true>, BicycleDyn<true> b; b.wheelbase = p.p[0]; b.inv_wheelbase = exact_inverse_pow2f(p.p[0]); b.lo[0] = p.p[1], b.hi[0] = p.p[2]; b.lo[1] = p.p[3], b.hi[1] = p.p[4]; return b;)
 ModelOps bc_fma_ops_ext() { return bc_fma_ops(); }
 }  // namespace smpc_dev
