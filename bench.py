@@ -11,13 +11,19 @@ samples, T = 100 (the large-sample sweep config the metric is quoted on for
 with the WorkerPool chunk rule).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--workload di|cartpole|diffdrive|quadrotor|autorally|bicycle] [--samples N]
-                  [--scaling strong|weak]
+                  [--workload di|cartpole|diffdrive|paper|quadrotor|autorally|bicycle] [--samples N]
+                  [--scaling strong|weak] [--comm single|exact] [--no-sweep]
 
-Rank 0 prints ONE JSON line. `value` = samples/s of the whole job from
-device-resident graph replays (CUDA events on the context stream, L2 flushed
-between steps, max over ranks); `e2e` = the same metric through the public
-C-ABI call `smpc_compute_control` with host x0 in and the host solution out.
+Rank 0 prints ONE JSON line (the last line of stdout). `value` = samples/s
+of the whole job from device-resident graph replays (CUDA events on the
+context stream, L2 flushed between steps, max over ranks); `e2e` = the same
+metric through the public C-ABI call `smpc_compute_control` with host x0 in
+and the host solution out. At N = 1 the line also carries `sweep`: every
+BASELINE.json config (and the reference's own bench_timing protocol over N),
+each with its device ms/iteration, e2e, rollout-kernel roofline and the
+reference CPU path (oracle/_ref) timed on this host at 1 thread and at all
+threads. `--gpus N` without torchrun re-launches itself under
+torch.distributed.run with N ranks.
 """
 import argparse
 import ctypes
@@ -46,13 +52,24 @@ from paper_2409_07563_b200 import scenario as S  # noqa: E402
 # Euler 14; tensor layer 2 = 32x32 MACs = 2048 flops (3xTF32 issues 3x that).
 # bicycle (C3, Ackermann): noise 58, control+clamp 6, derivative 5 (+4 sin/cos),
 # Euler 6, wrap 2, nav cost 16.
-FP32_OPS_PER_SAMPLE_STEP = {"di": 83, "cartpole": 56, "diffdrive": 90, "quadrotor": 214, "autorally": 718,
-                            "bicycle": 93}
-FP64_OPS_PER_SAMPLE_STEP = {"di": 9, "cartpole": 23, "diffdrive": 19, "quadrotor": 65, "autorally": 41,
-                            "bicycle": 19}
-TENSOR_FLOPS_PER_SAMPLE_STEP = {"autorally": 2048}
-# workloads whose model exists in the reference (oracle/_ref can time them)
-REFERENCE_WORKLOADS = ("di", "cartpole", "diffdrive")
+FP32_OPS_PER_SAMPLE_STEP = {"di": 83, "cartpole": 56, "diffdrive": 90, "paper": 90, "quadrotor": 214,
+                            "autorally": 718, "autorally_rmppi": 718, "bicycle": 93}
+FP64_OPS_PER_SAMPLE_STEP = {"di": 9, "cartpole": 23, "diffdrive": 19, "paper": 19, "quadrotor": 65,
+                            "autorally": 41, "autorally_rmppi": 41, "bicycle": 19}
+TENSOR_FLOPS_PER_SAMPLE_STEP = {"autorally": 2048, "autorally_rmppi": 2048}
+# workloads whose model exists in the reference (oracle/_ref can time them);
+# the others are builder-defined and timed on their restated C twin (1 thread)
+REFERENCE_WORKLOADS = ("di", "cartpole", "diffdrive", "paper")
+WORKLOADS = ("di", "cartpole", "diffdrive", "paper", "quadrotor", "autorally", "autorally_rmppi", "bicycle")
+METRIC = "rollout samples/s per MPPI iteration (compute_control, I=1)"
+# (workload, N) of the driver-visible sweep: every BASELINE.json config plus
+# the reference's own timing protocol (bench.cpp:178-185) over N
+SWEEP = [("cartpole", 2048), ("cartpole", 8192),
+         ("quadrotor", 128), ("quadrotor", 1024), ("quadrotor", 8192), ("quadrotor", 16384),
+         ("diffdrive", 2000), ("bicycle", 2000),
+         ("autorally", 8192),
+         ("di", 65536), ("di", 262144),
+         ("paper", 128), ("paper", 1024), ("paper", 2048), ("paper", 8192), ("paper", 16384)]
 
 
 def make_scenario(workload: str, n: int) -> S.Scenario:
@@ -62,12 +79,16 @@ def make_scenario(workload: str, n: int) -> S.Scenario:
         return S.cartpole_scenario(num_samples=n, horizon=100, seed=1)
     if workload == "diffdrive":
         return S.diff_drive_nav_scenario(num_samples=n, horizon=56, seed=42)
+    if workload == "paper":
+        return S.default_timing_scenario(num_samples=n)
     if workload == "quadrotor":
         return S.quadrotor_scenario(num_samples=n, horizon=100, seed=13)
     if workload == "bicycle":
         return S.bicycle_nav_scenario(num_samples=n, horizon=56, seed=42)
     if workload == "autorally":
         return S.autorally_scenario(num_samples=n, horizon=100, seed=21, controller="tube")
+    if workload == "autorally_rmppi":
+        return S.autorally_scenario(num_samples=n, horizon=100, seed=21, controller="rmppi")
     raise SystemExit(f"unknown workload {workload}")
 
 
@@ -75,6 +96,9 @@ def workload_name(workload: str, n: int) -> str:
     return {"di": f"C5 double_integrator+circle_track MPPI N={n} T=100",
             "cartpole": f"C1 cartpole+quadratic MPPI N={n} T=100",
             "diffdrive": f"C3 diff_drive+diff_drive_nav(costmap 110x110) MPPI N={n} T=56",
+            "paper": f"paper protocol (bench.cpp default_timing_scenario): diff_drive+diff_drive_nav "
+                     f"(empty 11 m map) sigma=0.2 MPPI N={n} T=100",
+            "autorally_rmppi": f"C4 AutoRally MLP dynamics (tcgen05) RMPPI N={n} T=100",
             "quadrotor": f"C2 quadrotor(13-state)+quadratic tracking MPPI N={n} T=100",
             "autorally": f"C4 AutoRally MLP dynamics (tcgen05) Tube-MPPI N={n} T=100",
             "bicycle": f"C3 Ackermann/bicycle+diff_drive_nav(costmap 110x110) MPPI N={n} T=56"}[workload]
@@ -135,10 +159,12 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def init_dist():
+def init_dist(want: int):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != want:
+        raise SystemExit(f"bench.py: --gpus {want} but WORLD_SIZE={world}")
     if world > 1:
         import torch
         import torch.distributed as dist
@@ -146,6 +172,21 @@ def init_dist():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         return rank, world, local, dist
     return 0, 1, 0, None
+
+
+def relaunch_under_torchrun(args) -> None:
+    """--gpus N without a torchrun environment: run this script as N ranks."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")          # rank counts of the communicator in the log
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    raise SystemExit(subprocess.call(cmd, env=env))
 
 
 def barrier(dist, local):
@@ -164,13 +205,36 @@ def max_over_ranks(dist, value: float) -> float:
     return float(t.item())
 
 
-def cpu_reference_run(sc, steps: int, warmup: int, budget_s: float, prefer_ref: bool = True):
+def host_info() -> dict:
+    """What the CPU reference ran on: cores, CPU model, glibc, compiler line."""
+    import platform
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        gxx = subprocess.run(["g++", "--version"], capture_output=True, text=True, timeout=10).stdout.split("\n")[0]
+    except (OSError, subprocess.TimeoutExpired):
+        gxx = None
+    return {"nproc": os.cpu_count(), "cpu_model": model, "glibc": " ".join(platform.libc_ver()),
+            "compiler": (gxx or "g++") + ": -std=c++20 -O3 -DNDEBUG -fPIC -ffp-contract=off "
+                        "(oracle/Makefile: reference core sources unmodified, no -march / -ffast-math)"}
+
+
+def cpu_reference_run(sc, steps: int, warmup: int, budget_s: float, prefer_ref: bool = True,
+                      workers: int = 0):
     """Time the reference's own compute_control on the host cores.
 
-    oracle/_ref (the unmodified reference, compiled here) with all host
-    threads when present; else the C restatement (single thread)."""
+    oracle/_ref (the unmodified reference, compiled here) with `workers`
+    threads (0 = all host threads) when present and the model exists in the
+    reference; else the C restatement (single thread)."""
     from oracle import bindings
-    ncores = os.cpu_count() or 1
+    ncores = workers or os.cpu_count() or 1
     if prefer_ref and bindings.ref_available():
         ctl = bindings.OracleController(sc, "reference", workers=ncores, strategy=1)
         kind, cores = "reference", ncores
@@ -178,38 +242,52 @@ def cpu_reference_run(sc, steps: int, warmup: int, budget_s: float, prefer_ref: 
         ctl = bindings.OracleController(sc, "port")
         kind, cores = "port", 1
     x0 = sc.x0()
+    comp = ctl.tube_compute_control if sc.controller == "tube" else (
+        ctl.rmppi_compute_control if sc.controller == "rmppi" else ctl.compute_control)
     for _ in range(warmup):
-        ctl.compute_control(x0)
+        comp(x0)
     times = []
     t_start = time.perf_counter()
     for _ in range(steps):
         t0 = time.perf_counter()
-        ctl.compute_control(x0)
+        comp(x0)
         times.append((time.perf_counter() - t0) * 1e3)
-        if time.perf_counter() - t_start > budget_s and len(times) >= 3:
+        if time.perf_counter() - t_start > budget_s and len(times) >= 1:
             break
     ms = statistics.mean(times)
     return {"kind": kind, "cores": cores, "ms": ms, "n": len(times),
             "value": sc.num_samples * 1000.0 / ms}
 
 
+def bench_config(workload: str, n_global: int, world: int, sc, comm: str) -> dict:
+    """The `config` object, identical in both arms."""
+    return {"workload": workload_name(workload, n_global), "samples": n_global,
+            "samples_per_gpu": n_global // world, "horizon": sc.horizon, "iterations": sc.iterations,
+            "parallelism": f"sample-shard dp{world}", "comm": comm if world > 1 else "none",
+            "l2": "flushed between timed steps (256 MiB write, outside the events)",
+            "update_skip_mass": sc.update_skip_mass,
+            "update_skip_rule": "update skips samples with e_m < update_skip_mass/M (contribution < "
+                                "skip_mass*max|eps|, below the fp32 rounding of U*); 0 = every sample"}
+
+
 def run_reference_arm(args):
-    rank, world, local, dist = init_dist()
+    rank, world, local, dist = init_dist(args.gpus)
     if rank != 0:
         return
-    sc = make_scenario(args.workload, args.samples)
+    n_global = args.samples * (world if args.scaling == "weak" else 1)
+    sc = make_scenario(args.workload, n_global)
     r = cpu_reference_run(sc, args.steps, args.warmup, budget_s=args.ref_budget,
                           prefer_ref=args.workload in REFERENCE_WORKLOADS)
     line = {
-        "metric": "rollout samples/s per MPPI iteration (compute_control, I=1)",
+        "metric": METRIC,
         "value": r["value"], "unit": "samples/s", "n_gpus": world, "steps": r["n"], "warmup": args.warmup,
         "ms_per_step": r["ms"], "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
         "dtype": "f32+f64", "data": "synthetic (seeded Philox noise, fixed x0)",
-        "config": {"workload": workload_name(args.workload, args.samples), "samples": args.samples,
-                   "horizon": sc.horizon, "iterations": 1},
+        "config": bench_config(args.workload, n_global, world, sc, args.comm),
         "impl": "reference",
         "cpu_baseline": {"value": r["value"], "unit": "samples/s", "cores": r["cores"], "kind": r["kind"],
-                         "sample": f"{r['n']} compute_control solves after {args.warmup} warm-ups, full N"},
+                         "sample": f"{r['n']} compute_control solves after {args.warmup} warm-ups, full N",
+                         "host": host_info()},
         "e2e": {"value": r["value"], "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -226,9 +304,139 @@ def load_traffic(workload: str, samples: int):
         return None
 
 
+def measured_bf16_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f).get("bf16_tflops")
+    except (OSError, ValueError):
+        return None
+
+
+def measure(ctl, sc, workload, n_global, shard, steps, warmup, roofline_steps, e2e_steps, device, flush, dist,
+            local, fp32_peak):
+    """Device-timed graph replays, rollout-kernel roofline and the e2e call."""
+    import torch
+    x0 = sc.x0()
+    stream = torch.cuda.ExternalStream(ctl.stream, device=torch.device("cuda", device))
+    ctl.set_x0(x0)
+    for _ in range(warmup):
+        ctl.launch_iteration()
+    ctl.synchronize()
+    barrier(dist, local)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    torch.cuda.synchronize()
+    barrier(dist, local)
+    for k in range(steps):
+        with torch.cuda.stream(stream):
+            flush.fill_(k & 0xFF)
+            starts[k].record(stream)
+        ctl.launch_iteration()
+        ends[k].record(stream)
+    ctl.synchronize()
+    torch.cuda.synchronize()
+    barrier(dist, local)
+    step_ms = [a.elapsed_time(b) for a, b in zip(starts, ends)]
+    ms_per_step = max_over_ranks(dist, float(sum(step_ms))) / steps
+
+    # rollout kernel alone (CUDA events on the context stream around each launch)
+    ctl.rollout_timing(True)
+    for k in range(roofline_steps):
+        flush.fill_(k & 0xFF)
+        torch.cuda.synchronize()
+        ctl.launch_iteration()
+        ctl.synchronize()
+    roll_ms_total, roll_n = ctl.rollout_timing(False)
+    roll_ms = roll_ms_total / max(roll_n, 1)
+    systems = 2 if sc.controller in ("tube", "rmppi") else 1
+    m_local = shard[1] - shard[0]
+    ops = m_local * sc.horizon * systems * FP32_OPS_PER_SAMPLE_STEP[workload]
+    achieved = ops / (roll_ms * 1e-3) / 1e12
+    roof = {"bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
+            "frac": achieved / fp32_peak if fp32_peak else None,
+            # the same FP32 op count against the FMA-counted nominal (2 flops per lane-cycle)
+            "frac_fma_counted": achieved / (2 * fp32_peak) if fp32_peak else None,
+            "traffic": load_traffic(workload, n_global),
+            "kernel": "mlp_rollout_kernel (tcgen05)" if workload.startswith("autorally") else "rollout_kernel",
+            "kernel_ms": roll_ms, "kernel_share_of_step": roll_ms / ms_per_step,
+            "peak_source": "measured in-run: FADD/FMUL issue-rate probe (no FMA: reference semantics)",
+            "algorithmic": f"{FP32_OPS_PER_SAMPLE_STEP[workload]} FP32 ops + {FP64_OPS_PER_SAMPLE_STEP[workload]} "
+                           f"FP64 ops per sample-step x {m_local} samples x {sc.horizon} steps"
+                           + (f" x {systems} systems" if systems > 1 else "") + " per launch",
+            "hbm_peak_gbs_measured": None}
+    if workload in TENSOR_FLOPS_PER_SAMPLE_STEP:
+        # tcgen05 layer: algorithmic TF32 flops / rollout time vs the dense TF32 peak
+        # (half the measured bf16 peak in MEASURED_PEAKS.json; B200_PROFILING.md fallback 1125 TF/s)
+        tf = m_local * sc.horizon * systems * TENSOR_FLOPS_PER_SAMPLE_STEP[workload]
+        bf16 = measured_bf16_peak()
+        tpeak = bf16 / 2 if bf16 else 1125.0
+        roof["tensor"] = {"achieved": tf / (roll_ms * 1e-3) / 1e12, "peak": tpeak, "unit": "TFLOP/s (tf32)",
+                          "frac": tf / (roll_ms * 1e-3) / 1e12 / tpeak,
+                          "algorithmic": f"{TENSOR_FLOPS_PER_SAMPLE_STEP[workload]} flops per sample-step "
+                                         "(32x32 layer; 3xTF32 issues 3 MMAs per product)"}
+
+    # e2e: public C-ABI call with host buffers (H2D x0, D2H solution)
+    barrier(dist, local)
+    e2e_steps = max(3, e2e_steps)
+    comp = ctl.tube_compute_control if systems == 2 else ctl.compute_control
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        comp(x0)
+    e2e_ms = max_over_ranks(dist, time.perf_counter() - t0) * 1e3 / e2e_steps
+    n_x, n_u, n_y = sc.dims
+    d2h = systems * 4 * (sc.horizon * n_u + (sc.horizon + 1) * n_x + sc.horizon * n_y) + 128
+    e2e = {"value": n_global * 1000.0 / e2e_ms, "unit": "samples/s", "ms_per_step": e2e_ms,
+           "h2d_bytes_per_step": 4 * n_x, "d2h_bytes_per_step": d2h,
+           "api": "smpc_tube_compute_control" if systems == 2 else
+                  "smpc_compute_control (MppiController::compute_control)"}
+    return {"ms_per_step": ms_per_step, "value": n_global * 1000.0 / ms_per_step, "step_ms": step_ms,
+            "roofline": roof, "e2e": e2e, "launches": ctl.kernels_per_solve * steps}
+
+
+def run_sweep(args, device, flush, fp32_peak):
+    """Every BASELINE config (+ the reference's timing protocol over N) on one
+    GPU, with the reference CPU path on this host at 1 thread and all threads."""
+    from paper_2409_07563_b200.controllers import make_controller
+    out = []
+    for workload, n in SWEEP:
+        sc = make_scenario(workload, n)
+        sc.device = device
+        ctl = make_controller(sc)
+        small = n <= 16384
+        r = measure(ctl, sc, workload, n, (0, n), steps=200 if small else 50, warmup=10, roofline_steps=20,
+                    e2e_steps=100 if small else 30, device=device, flush=flush, dist=None, local=0,
+                    fp32_peak=fp32_peak)
+        ctl.close()
+        ent = {"workload": workload_name(workload, n), "key": f"{workload}:{n}", "samples": n,
+               "horizon": sc.horizon, "ms_per_iter": r["ms_per_step"], "samples_per_s": r["value"],
+               "p50_ms": statistics.median(r["step_ms"]), "p99_ms": float(np.percentile(r["step_ms"], 99)),
+               "e2e_ms": r["e2e"]["ms_per_step"], "rollout_ms": r["roofline"]["kernel_ms"],
+               "rollout_frac_fp32_issue": r["roofline"]["frac"], "gpu_launches_per_iter": r["launches"] // 200
+               if small else r["launches"] // 50}
+        if "tensor" in r["roofline"]:
+            ent["tensor_tf32_tflops"] = r["roofline"]["tensor"]["achieved"]
+            ent["tensor_frac"] = r["roofline"]["tensor"]["frac"]
+        if not args.no_cpu_baseline:
+            ref = workload in REFERENCE_WORKLOADS
+            cpu = {}
+            for w in ([1, 0] if ref else [1]):
+                c = cpu_reference_run(sc, steps=5, warmup=1, budget_s=args.sweep_cpu_budget, prefer_ref=ref,
+                                      workers=w)
+                cpu[f"w{c['cores']}"] = {"ms_per_iter": c["ms"], "samples_per_s": c["value"], "kind": c["kind"],
+                                         "solves": c["n"]}
+            ent["cpu"] = cpu
+            best = min(v["ms_per_iter"] for v in cpu.values())
+            ent["speedup_e2e_vs_best_cpu"] = best / r["e2e"]["ms_per_step"]
+            if not ref:
+                ent["cpu_note"] = "builder-defined model: no reference implementation; CPU figure is its " \
+                                  "restated C twin (oracle port, 1 thread), parity unpinned"
+        out.append(ent)
+    return out
+
+
 def run_ours(args):
     import torch
-    rank, world, local, dist = init_dist()
+    rank, world, local, dist = init_dist(args.gpus)
     from paper_2409_07563_b200 import _lib
     from paper_2409_07563_b200.controllers import make_controller
 
@@ -240,6 +448,7 @@ def run_ours(args):
     shard = S.shard_range(n_global, rank, world)
     ctl = make_controller(sc, shard=shard)
     if world > 1:
+        ctl.comm_set_mode(args.comm)
         uid = bytes(128)
         if rank == 0:
             buf = ctypes.create_string_buffer(128)
@@ -248,118 +457,50 @@ def run_ours(args):
         obj = [uid]
         dist.broadcast_object_list(obj, src=0)
         ctl.comm_init(obj[0], rank, world)
-    x0 = sc.x0()
-    stream = torch.cuda.ExternalStream(ctl.stream, device=torch.device("cuda", device))
     # L2 flush buffer (> 126 MB L2): written between timed steps, outside the events.
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=f"cuda:{device}")
-
-    ctl.set_x0(x0)
-    for _ in range(args.warmup):
-        ctl.launch_iteration()
-    ctl.synchronize()
-    barrier(dist, local)
-
-    # ---- timed region: device-resident graph replays --------------------------
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    with ClockSampler(device) as clocks:
-        torch.cuda.synchronize()
-        barrier(dist, local)
-        for k in range(args.steps):
-            with torch.cuda.stream(stream):
-                flush.fill_(k & 0xFF)
-                starts[k].record(stream)
-            ctl.launch_iteration()
-            ends[k].record(stream)
-        ctl.synchronize()
-        torch.cuda.synchronize()
-        barrier(dist, local)
-    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    total_ms = max_over_ranks(dist, float(sum(step_ms)))
-    ms_per_step = total_ms / args.steps
-    value = n_global * 1000.0 / ms_per_step
-    launches = ctl.kernels_per_solve * args.steps
-
-    # ---- roofline: rollout kernel alone (CUDA events around each launch) -----
-    ctl.rollout_timing(True)
-    for k in range(args.roofline_steps):
-        flush.fill_(k & 0xFF)
-        torch.cuda.synchronize()
-        ctl.launch_iteration()
-        ctl.synchronize()
-    roll_ms_total, roll_n = ctl.rollout_timing(False)
-    roll_ms = roll_ms_total / max(roll_n, 1)
-    systems = 2 if sc.controller == "tube" else 1
-    ops_per_launch = (shard[1] - shard[0]) * sc.horizon * systems * FP32_OPS_PER_SAMPLE_STEP[args.workload]
     peak = ctypes.c_double()
     _lib.load().smpc_measure_fp32_peak(device, ctypes.byref(peak))
-    achieved = ops_per_launch / (roll_ms * 1e-3) / 1e12
-    roofline = {"bound": "fp32", "achieved": achieved, "peak": peak.value, "unit": "TFLOP/s",
-                "frac": achieved / peak.value if peak.value else None,
-                "traffic": load_traffic(args.workload, n_global),
-                "kernel": "rollout_kernel", "kernel_ms": roll_ms,
-                "kernel_share_of_step": roll_ms / ms_per_step,
-                "peak_source": "measured in-run: FADD/FMUL issue-rate probe (no FMA: reference semantics)",
-                "algorithmic": f"{FP32_OPS_PER_SAMPLE_STEP[args.workload]} FP32 ops + "
-                               f"{FP64_OPS_PER_SAMPLE_STEP[args.workload]} FP64 ops per sample-step "
-                               f"x {shard[1] - shard[0]} samples x {sc.horizon} steps per launch",
-                "hbm_peak_gbs_measured": None}
-    if args.workload in TENSOR_FLOPS_PER_SAMPLE_STEP:
-        # tcgen05 layer: algorithmic TF32 flops / rollout time vs the dense TF32 peak
-        # (half the measured bf16 peak in MEASURED_PEAKS.json; B200_PROFILING.md fallback 1125 TF/s)
-        tf = (shard[1] - shard[0]) * sc.horizon * systems * TENSOR_FLOPS_PER_SAMPLE_STEP[args.workload]
-        bf16 = None
-        try:
-            with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-                bf16 = json.load(f).get("bf16_tflops")
-        except (OSError, ValueError):
-            pass
-        tpeak = bf16 / 2 if bf16 else 1125.0
-        roofline["tensor"] = {"achieved": tf / (roll_ms * 1e-3) / 1e12, "peak": tpeak, "unit": "TFLOP/s (tf32)",
-                              "frac": tf / (roll_ms * 1e-3) / 1e12 / tpeak,
-                              "algorithmic": f"{TENSOR_FLOPS_PER_SAMPLE_STEP[args.workload]} flops per sample-step "
-                                             "(32x32 layer; 3xTF32 issues 3 MMAs per product)"}
 
-    # ---- e2e: public C-ABI call with host buffers (H2D x0, D2H solution) -----
-    barrier(dist, local)
-    e2e_steps = max(3, min(args.steps, args.e2e_steps))
-    t0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        ctl.compute_control(x0)
-    e2e_s = max_over_ranks(dist, time.perf_counter() - t0)
-    e2e_ms = e2e_s * 1e3 / e2e_steps
-    n_x, n_u, n_y = sc.dims
-    d2h = systems * 4 * (sc.horizon * n_u + (sc.horizon + 1) * n_x + sc.horizon * n_y) + 128
-    e2e = {"value": n_global * 1000.0 / e2e_ms, "unit": "samples/s", "ms_per_step": e2e_ms,
-           "h2d_bytes_per_step": 4 * n_x, "d2h_bytes_per_step": d2h,
-           "api": "smpc_compute_control (MppiController::compute_control)"}
+    with ClockSampler(device) as clocks:
+        r = measure(ctl, sc, args.workload, n_global, shard, args.steps, args.warmup, args.roofline_steps,
+                    min(args.steps, args.e2e_steps), device, flush, dist, local, peak.value)
+    ctl.close()
 
     cpu = None
+    sweep = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        r = cpu_reference_run(sc, steps=args.cpu_steps, warmup=1, budget_s=args.cpu_budget,
+        c = cpu_reference_run(sc, steps=args.cpu_steps, warmup=1, budget_s=args.cpu_budget,
                               prefer_ref=args.workload in REFERENCE_WORKLOADS)
-        cpu = {"value": r["value"], "unit": "samples/s", "cores": r["cores"], "kind": r["kind"],
-               "ms_per_step": r["ms"],
-               "sample": f"{r['n']} full-size compute_control solves (N={n_global}) after 1 warm-up"}
+        c1 = cpu_reference_run(sc, steps=1, warmup=0, budget_s=args.cpu_budget,
+                               prefer_ref=args.workload in REFERENCE_WORKLOADS, workers=1)
+        cpu = {"value": c["value"], "unit": "samples/s", "cores": c["cores"], "kind": c["kind"],
+               "ms_per_step": c["ms"],
+               "sample": f"{c['n']} full-size compute_control solves (N={n_global}) after 1 warm-up",
+               "single_thread": {"value": c1["value"], "ms_per_step": c1["ms"], "cores": c1["cores"],
+                                 "kind": c1["kind"], "sample": f"{c1['n']} full-size solve(s), no warm-up"},
+               "host": host_info()}
+    if rank == 0 and world == 1 and not args.no_sweep:
+        sweep = run_sweep(args, device, flush, peak.value)
 
     if rank == 0:
         clk = clocks.summary()
         line = {
-            "metric": "rollout samples/s per MPPI iteration (compute_control, I=1)",
-            "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": args.scaling,
+            "metric": METRIC,
+            "value": r["value"], "unit": "samples/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "f32+f64",
             "data": "synthetic (seeded Philox noise regenerated in-kernel, fixed x0)",
-            "config": {"workload": workload_name(args.workload, n_global), "samples": n_global,
-                       "samples_per_gpu": shard[1] - shard[0], "horizon": sc.horizon, "iterations": 1,
-                       "parallelism": f"sample-shard dp{world}",
-                       "l2": "flushed between timed steps (256 MiB write, outside the events)"},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "config": bench_config(args.workload, n_global, world, sc, args.comm),
+            "roofline": r["roofline"], "cpu_baseline": cpu, "e2e": r["e2e"], "gpu_launches": r["launches"],
             "clocks": {"sm_mhz": clk["sm_mhz"], "sm_max_mhz": clk["sm_max_mhz"], "reasons": clk["reasons"]},
-            "p50_ms": statistics.median(step_ms), "p99_ms": float(np.percentile(step_ms, 99)),
+            "p50_ms": statistics.median(r["step_ms"]), "p99_ms": float(np.percentile(r["step_ms"], 99)),
+            "comm": {"nranks": world, "mode": args.comm if world > 1 else "none",
+                     "collectives_per_iteration": (1 if args.comm == "single" else 3) if world > 1 else 0},
         }
+        if sweep is not None:
+            line["sweep"] = sweep
         print(json.dumps(line), flush=True)
-    ctl.close()
     if dist is not None:
         dist.destroy_process_group()
 
@@ -370,17 +511,21 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="di", choices=["di", "cartpole", "diffdrive", "quadrotor", "autorally",
-                                                           "bicycle"])
+    ap.add_argument("--workload", default="di", choices=list(WORKLOADS))
     ap.add_argument("--samples", type=int, default=1 << 20)
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
+    ap.add_argument("--comm", default="single", choices=["single", "exact"])
     ap.add_argument("--roofline-steps", type=int, default=20)
     ap.add_argument("--e2e-steps", type=int, default=100)
     ap.add_argument("--cpu-steps", type=int, default=5)
     ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--sweep-cpu-budget", type=float, default=3.0)
     ap.add_argument("--ref-budget", type=float, default=120.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch_under_torchrun(args)
     if args.impl == "reference":
         run_reference_arm(args)
     else:

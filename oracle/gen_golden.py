@@ -58,6 +58,28 @@ def fixture_scenarios():
     tube = S.cartpole_scenario(num_samples=256, horizon=50, seed=4)
     tube.controller = "tube"
     sc["cartpole_tube"] = tube
+    # iterations > 1 (controllers.cpp:115-131): stream_for(iter) and the mean
+    # updated between the in-solve iterations
+    it3 = S.cartpole_scenario(num_samples=256, horizon=60, seed=21)
+    it3.iterations = 3
+    sc["cartpole_iter3"] = it3
+    # DMD with per-step gamma (engine.cpp:397-401) and I = 3
+    sc["di_dmd_perstep_iter3"] = S.Scenario(num_samples=192, horizon=25, dynamics="double_integrator",
+                                            cost="quadratic", target=[1.0, -1.0, 0.0, 0.0],
+                                            weights=[1.0, 1.0, 0.1, 0.1], rng_seed=31, control_std=(0.7, 0.4),
+                                            controller="dmd", iterations=3, lambda_=0.7,
+                                            step_size_per_step=[0.3 + 0.025 * t for t in range(25)])
+    tube3 = S.cartpole_scenario(num_samples=256, horizon=40, seed=23)
+    tube3.controller, tube3.iterations = "tube", 3
+    sc["cartpole_tube_iter3"] = tube3
+    cem3 = S.di_swarm_scenario(num_samples=200, horizon=30, seed=25)
+    cem3.controller, cem3.elite_fraction, cem3.iterations = "cem", 0.1, 3
+    sc["di_cem_iter3"] = cem3
+    # C3 with sigma = 0.2 (non-power-of-two sigma^2: the importance term divides)
+    # and I = 2, over the reference's own obstacles.costmap
+    nav2 = S.diff_drive_nav_scenario(num_samples=200, horizon=56, seed=44, costmap=S.Costmap.load(OBSTACLES))
+    nav2.iterations, nav2.lambda_ = 2, 0.3
+    sc["diffdrive_nav_sigma02_iter2"] = nav2
     return sc
 
 
@@ -75,12 +97,19 @@ def scenario_record(sc: S.Scenario) -> dict:
     return d
 
 
-def main():
+def main(only=None):
+    """Regenerate every fixture, or only the named ones (index.json is merged)."""
     build()
     R = Oracle("reference")
     os.makedirs(OUT, exist_ok=True)
     index = {}
+    old = None
+    if only:
+        old = json.load(open(os.path.join(OUT, "index.json")))
+        index = old["scenarios"]
     for name, sc in fixture_scenarios().items():
+        if only and name not in only:
+            continue
         n_x, n_u, n_y = sc.dims
         T = sc.horizon
         rng = np.random.default_rng(zlib.crc32(name.encode()))
@@ -132,13 +161,15 @@ def main():
     # Closed loops: the reference's own Plant::run_control_loop (plant.cpp:133-181).
     from oracle.bindings import reference_control_loop
     for name, (sc, steps) in closed_loop_scenarios().items():
+        if only and name not in only:
+            continue
         acc, rows = reference_control_loop(sc, steps * sc.dt)
         np.savez_compressed(os.path.join(OUT, f"{name}.npz"), accumulated_cost=np.float64(acc), rows=rows,
                             steps=np.int64(steps))
         index[name] = scenario_record(sc)
         print(name, "accumulated cost", acc)
     # Random123 Philox4x32-10 known-answer vectors and reference normals.
-    kat = {
+    kat = old["kat"] if old else {
         "philox": [
             [[0, 0, 0, 0], [0, 0], [int(v) for v in R.philox([0, 0, 0, 0], [0, 0])]],
             [[0xFFFFFFFF] * 4, [0xFFFFFFFF] * 2, [int(v) for v in R.philox([0xFFFFFFFF] * 4, [0xFFFFFFFF] * 2)]],
@@ -156,4 +187,4 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    main(set(sys.argv[1:]) or None)

@@ -260,6 +260,10 @@ class MppiController(RolloutEngine):
     def comm_init(self, unique_id: bytes, rank: int, world: int) -> None:
         self._check(self.lib.smpc_comm_init(self.ctx, unique_id, rank, world))
 
+    def comm_set_mode(self, mode: str) -> None:
+        """"single" (default): one all-gather per iteration; "exact": three."""
+        self._check(self.lib.smpc_comm_set_mode(self.ctx, COMM_MODES[mode]))
+
 
 class TubeMppiController(MppiController):
     """TubeMppiController: nominal + real systems share one noise batch."""
@@ -276,6 +280,9 @@ class TubeMppiController(MppiController):
 
     def compute_control(self, x0, want_weights: bool = False) -> ControllerSolution:
         return self.tube_compute_control(x0, want_weights).nominal
+
+
+COMM_MODES = {"exact": 0, "single": 1}
 
 
 def make_controller(scenario: Scenario, shard: Optional[tuple] = None) -> MppiController:
@@ -297,7 +304,7 @@ class ShardGroup:
     device-to-device copies standing in for NCCL. devices: one ordinal per
     shard (default: all on the scenario's device)."""
 
-    def __init__(self, scenario: Scenario, n: int, devices=None):
+    def __init__(self, scenario: Scenario, n: int, devices=None, mode: str = "single"):
         self.n = n
         self.members = []
         for r in range(n):
@@ -305,6 +312,7 @@ class ShardGroup:
             if devices is not None:
                 sc.device = devices[r]
             self.members.append(MppiController(sc, shard_range(scenario.num_samples, r, n)))
+            self.members[-1].comm_set_mode(mode)
         self.lib = self.members[0].lib
         self._arr = (ctypes.c_void_p * n)(*[m.ctx.value for m in self.members])
         check(self.lib.smpc_group_init(self._arr, n), self.members[0].ctx)

@@ -256,4 +256,61 @@ GM_HD float cosf_glibc(float y) {
   return u2f(0x7fc00000u);
 }
 
+// sinf and cosf of the same argument with ONE range reduction (the
+// state_derivatives call both, dynamics.cpp:128-129, :144-145, :168-169).
+// Same branches, same reduction, then the two polynomial evaluations of
+// sinf_glibc / cosf_glibc: equal to the separate ports by construction and
+// checked exhaustively (smpc_libm_hash rows 3-4 against the host libm).
+template <bool FMA>
+GM_HD void sincosf_glibc(float y, float* sp, float* cp) {
+  double x = y;
+  const SincosfTable* p = &GM_SINCOSF_TAB[0];
+  int n;
+  if (abstop12(y) < abstop12(0x1.921fb6p-1f)) {
+    const double x2 = GM_DMUL(x, x);
+    if (abstop12(y) < abstop12(0x1p-12f)) {
+      *sp = y;
+      *cp = 1.0f;
+      return;
+    }
+    *sp = sinf_poly<FMA>(x, x2, p, 0);
+    *cp = sinf_poly<FMA>(x, x2, p, 1);
+    return;
+  }
+  if (abstop12(y) < abstop12(120.0f)) {
+    x = reduce_fast<FMA>(x, p, &n);
+    const double s = p->sign[n & 3];
+    if (n & 2) p = &GM_SINCOSF_TAB[1];
+    const double xs = GM_DMUL(x, s), xx = GM_DMUL(x, x);
+    *sp = sinf_poly<FMA>(xs, xx, p, n);
+    *cp = sinf_poly<FMA>(xs, xx, p, n ^ 1);
+    return;
+  }
+  if (abstop12(y) < 0x7f8u) {
+    const uint32_t xi = f2u(y);
+    const int sign = xi >> 31;
+    x = reduce_large(xi, &n);
+    const double s = p->sign[(n + sign) & 3];
+    if ((n + sign) & 2) p = &GM_SINCOSF_TAB[1];
+    const double xs = GM_DMUL(x, s), xx = GM_DMUL(x, x);
+    *sp = sinf_poly<FMA>(xs, xx, p, n);
+    *cp = sinf_poly<FMA>(xs, xx, p, n ^ 1);
+    return;
+  }
+  *sp = *cp = u2f(0x7fc00000u);
+}
+
+// Order-independent fingerprint of a function over all 2^32 float inputs
+// (test infrastructure: the device result is compared with the same sum over
+// the host libm, tests/golden/libm_hash.json). NaN outputs hash as the
+// canonical quiet NaN; the sum is bucketed by the input's top 8 bits so a
+// mismatch names a 2^24-wide input range.
+GM_HD uint64_t libm_hash_term(uint32_t in, float out) {
+  const uint32_t bits = out != out ? 0x7fc00000u : f2u(out);
+  uint64_t z = (((uint64_t)in << 32) | bits) + 0x9E3779B97F4A7C15ULL;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
 }  // namespace smpc_glibc

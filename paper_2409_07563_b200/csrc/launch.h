@@ -185,6 +185,11 @@ struct IterArgs {
   double* blk_part;      // [S][QG][upd_slots][QW][4] per-warp quad sums, by rank among the group's warps
   int upd_slots;         // max warps covering one quad group
   double* gather3;       // [world][S][T*NU]
+  // per-rank strides (doubles) of gather1/2/3: separate buffers in the exact
+  // three-collective mode; one packed record [g1 | g2 | g3] per rank in the
+  // single-collective mode (one ncclAllGather per iteration)
+  int g1s, g2s, g3s;
+  int comm_single;        // single-collective mode: local baselines + rescaled combine
   // results
   ResultHeader* header;
   float* controls;  // [S][T][NU]

@@ -396,7 +396,7 @@ __global__ void __launch_bounds__(kTile, 4) mlp_rollout_kernel(const IterArgs a,
     }
     block_argmin<kTile>(j, mm);
     if (tid == 0) {
-      double* g = a.gather1 + ((size_t)a.rank * a.S + s) * 2;
+      double* g = a.gather1 + (size_t)a.rank * a.g1s + s * 2;
       g[0] = j;
       g[1] = __longlong_as_double(mm);
     }

@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(256) select_mark_kernel(const IterArgs a, cons
       run += ((volatile int*)a.cand_cnt)[b];
     }
     a.cand_off[gridDim.x] = run;
-    double* g = a.gather2 + (size_t)a.rank * a.S * 2;
+    double* g = a.gather2 + (size_t)a.rank * a.g2s;
     g[0] = 1.0;              // eta for the update: w_m = e_m / 1 = 1 exactly
     g[1] = (double)st->k;    // elites ("nonzero" weights)
   }

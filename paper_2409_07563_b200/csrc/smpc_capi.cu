@@ -154,6 +154,8 @@ struct smpc_ctx {
   // multi-GPU
   ncclComm_t comm = nullptr;
   int rank = 0, world = 1;
+  int comm_mode = SMPC_COMM_SINGLE;  // one all-gather per iteration (smpc_comm_set_mode)
+  double* d_gather_rec = nullptr;    // [8][rec] packed per-rank records of the single-collective mode
   // host state
   uint64_t solve_count = 0;
   std::string err;
@@ -344,6 +346,8 @@ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 uint32_t tail_table_size(uint32_t* j_lo_out, uint32_t* j_hi_out);
 
+int gather_record(const smpc_ctx* c) { return 4 * c->S + c->S * c->T * c->nu; }
+
 void fill_args(smpc_ctx* c) {
   IterArgs& a = c->base;
   const smpc_problem& p = c->p;
@@ -418,6 +422,18 @@ void fill_args(smpc_ctx* c) {
   a.n_u_blocks = c->n_u_blocks;
   a.blk_part = c->d_blk_part;
   a.gather3 = c->d_gather3;
+  a.comm_single = c->comm_mode == SMPC_COMM_SINGLE;
+  if (a.comm_single) {  // one record per rank: [S][2] (rho, argmin) | [S][2] (eta, nz) | [S][T*NU] sums
+    const int rec = gather_record(c);
+    a.gather1 = c->d_gather_rec;
+    a.gather2 = c->d_gather_rec + 2 * c->S;
+    a.gather3 = c->d_gather_rec + 4 * c->S;
+    a.g1s = a.g2s = a.g3s = rec;
+  } else {
+    a.g1s = 2 * c->S;
+    a.g2s = 2 * c->S;
+    a.g3s = c->S * c->T * c->nu;
+  }
   a.header = c->header();
   a.controls = reinterpret_cast<float*>(c->d_result + c->off_controls);
   a.states = reinterpret_cast<float*>(c->d_result + c->off_states);
@@ -558,22 +574,29 @@ void enqueue_solve(smpc_ctx* c, bool timed) {
       CK(c->ops.update(a, c->stream));
       continue;
     }
-    if (c->world > 1) {
+    const bool single = c->comm_mode == SMPC_COMM_SINGLE;
+    if (c->world > 1 && !single) {
       const size_t n1 = (size_t)c->S * 2;
       if (nccl()->AllGather(c->d_gather1 + c->rank * n1, c->d_gather1, n1, ncclFloat64, c->comm, c->stream))
         throw CudaError{"ncclAllGather (rho) failed"};
     }
     CK(c->ops.weights(a, c->stream));
-    if (c->world > 1) {
+    if (c->world > 1 && !single) {
       const size_t n2 = (size_t)c->S * 2;
       if (nccl()->AllGather(c->d_gather2 + c->rank * n2, c->d_gather2, n2, ncclFloat64, c->comm, c->stream))
         throw CudaError{"ncclAllGather (eta) failed"};
     }
     CK(c->ops.update(a, c->stream));
     if (c->world > 1) {
-      const size_t n3 = (size_t)c->S * c->T * c->nu;
-      if (nccl()->AllGather(c->d_gather3 + c->rank * n3, c->d_gather3, n3, ncclFloat64, c->comm, c->stream))
-        throw CudaError{"ncclAllGather (weighted sums) failed"};
+      if (single) {  // (rho_g, argmin_g, eta_g, nz_g, S_g) of every rank in one collective
+        const size_t n = (size_t)gather_record(c);
+        if (nccl()->AllGather(c->d_gather_rec + c->rank * n, c->d_gather_rec, n, ncclFloat64, c->comm, c->stream))
+          throw CudaError{"ncclAllGather (iteration record) failed"};
+      } else {
+        const size_t n3 = (size_t)c->S * c->T * c->nu;
+        if (nccl()->AllGather(c->d_gather3 + c->rank * n3, c->d_gather3, n3, ncclFloat64, c->comm, c->stream))
+          throw CudaError{"ncclAllGather (weighted sums) failed"};
+      }
       CK(c->ops.combine(a, c->stream));
     }
   }
@@ -595,7 +618,10 @@ void group_allgather(smpc_ctx** cs, int n, int which) {
       CK(cudaStreamWaitEvent(dst->stream, src->ev_stage, 0));
       size_t slot;
       double *from, *to;
-      if (which == 1) {
+      if (which == 0) {  // single-collective record
+        slot = (size_t)gather_record(src);
+        from = src->d_gather_rec, to = dst->d_gather_rec;
+      } else if (which == 1) {
         slot = (size_t)src->S * 2;
         from = src->d_gather1, to = dst->d_gather1;
       } else if (which == 2) {
@@ -620,12 +646,13 @@ void enqueue_group_solve(smpc_ctx** cs, int n) {
       a.do_finish = it == I - 1;
       return a;
     };
+    const bool single = cs[0]->comm_mode == SMPC_COMM_SINGLE;
     for (int r = 0; r < n; ++r) CK(cs[r]->ops.rollout(args(cs[r]), cs[r]->p.cost_kind, cs[r]->stream));
-    group_allgather(cs, n, 1);
+    if (!single) group_allgather(cs, n, 1);
     for (int r = 0; r < n; ++r) CK(cs[r]->ops.weights(args(cs[r]), cs[r]->stream));
-    group_allgather(cs, n, 2);
+    if (!single) group_allgather(cs, n, 2);
     for (int r = 0; r < n; ++r) CK(cs[r]->ops.update(args(cs[r]), cs[r]->stream));
-    group_allgather(cs, n, 3);
+    group_allgather(cs, n, single ? 0 : 3);
     for (int r = 0; r < n; ++r) CK(cs[r]->ops.combine(args(cs[r]), cs[r]->stream));
   }
   for (int r = 0; r < n; ++r) CK(launch_finish_solve(cs[r]->header(), cs[r]->stream));
@@ -887,6 +914,7 @@ smpc_status smpc_create(const smpc_problem* problem, smpc_ctx** out) {
     c->d_gather1 = dalloc<double>((size_t)c->S * 2 * 8);
     c->d_gather2 = dalloc<double>((size_t)c->S * 2 * 8);
     c->d_gather3 = dalloc<double>((size_t)c->S * TU * 8);
+    c->d_gather_rec = dalloc<double>((size_t)gather_record(c) * 8);
     // result region: header | controls | states | outputs
     size_t off = align_up(sizeof(ResultHeader), 256);
     c->off_controls = off;
@@ -1143,7 +1171,10 @@ smpc_status smpc_shift_control_sequence(smpc_ctx* c, double elapsed_s, double dt
     const int T = c->T, nu = c->nu;
     std::vector<float> m((size_t)T * nu), shifted((size_t)T * nu);
     for (int s = 0; s < c->S; ++s) {
-      CK(cudaMemcpy(m.data(), c->d_mean + (size_t)s * T * nu, sizeof(float) * T * nu, cudaMemcpyDeviceToHost));
+      // on the context stream: ordered after a graph left running by smpc_launch_iteration
+      CK(cudaMemcpyAsync(m.data(), c->d_mean + (size_t)s * T * nu, sizeof(float) * T * nu, cudaMemcpyDeviceToHost,
+                         c->stream));
+      CK(cudaStreamSynchronize(c->stream));
       if (steps >= T) {
         std::fill(shifted.begin(), shifted.end(), 0.f);
       } else {
@@ -1152,7 +1183,9 @@ smpc_status smpc_shift_control_sequence(smpc_ctx* c, double elapsed_s, double dt
           for (int u = 0; u < nu; ++u) shifted[t * nu + u] = m[src * nu + u];
         }
       }
-      CK(cudaMemcpy(c->d_mean + (size_t)s * T * nu, shifted.data(), sizeof(float) * T * nu, cudaMemcpyHostToDevice));
+      CK(cudaMemcpyAsync(c->d_mean + (size_t)s * T * nu, shifted.data(), sizeof(float) * T * nu, cudaMemcpyHostToDevice,
+                         c->stream));
+      CK(cudaStreamSynchronize(c->stream));
     }
   });
 }
@@ -1222,6 +1255,10 @@ smpc_status smpc_rollout(smpc_ctx* c, int32_t S, const float* x0s, const float* 
     a.blk_arg = blk_arg;
     a.rank = 0;
     a.world = 1;
+    // RolloutEngine::rollout takes its cost adjustments from the sampler
+    // config whatever controller owns the engine (only CemController's own
+    // compute_control drops them, controllers.cpp:155-162)
+    a.importance = c->p.importance_sampling != 0;
     if (eps) {
       const size_t n = (size_t)c->M_local * TU;
       if (c->eps_cap < n) {
@@ -1308,6 +1345,8 @@ smpc_status smpc_compute_weights(smpc_ctx* c, const double* costs, int64_t count
     a.blk_nz = reinterpret_cast<long long*>(d_nz);
     a.cand = d_cand;
     a.cand_e = nullptr;  // weights only: no update follows
+    a.cem_k = 0.0;       // plain softmin weights e/eta even on a CEM context (engine.cpp:342-363)
+    a.skip_w = 0.0;
     a.cand_cnt = d_ccnt;
     a.cand_off = d_coff;
     CK(launch_weights(a, c->stream));
@@ -1382,6 +1421,10 @@ smpc_status smpc_export_sample_trajectories(smpc_ctx* c, const float* x0, const 
     a.x0 = c->d_ro_x0;
     a.rank = 0;
     a.world = 1;
+    // RolloutEngine::rollout takes its cost adjustments from the sampler
+    // config whatever controller owns the engine (only CemController's own
+    // compute_control drops them, controllers.cpp:155-162)
+    a.importance = c->p.importance_sampling != 0;
     if (eps) {
       const size_t n = (size_t)c->M_local * TU;
       if (c->eps_cap < n) {
@@ -1531,7 +1574,12 @@ smpc_status smpc_group_init(smpc_ctx** ctxs, int32_t n) {
     for (int r = 0; r < n; ++r) {
       smpc_ctx* c = ctxs[r];
       if (n > 1 && c->p.controller_kind == SMPC_CTRL_CEM) throw ConfigError{"cem: multi-GPU sharding is not supported"};
-      if (c->M != ctxs[0]->M || c->T != ctxs[0]->T || c->S != ctxs[0]->S || c->I != ctxs[0]->I)
+      // the in-process group runs plain compute_control solves: no per-solve
+      // nominal-state choice (RMPPI) and no Tube nominal bookkeeping
+      if (c->p.controller_kind == SMPC_CTRL_RMPPI || c->p.controller_kind == SMPC_CTRL_TUBE)
+        throw ConfigError{"smpc_group_init: tube and rmppi controllers are not supported by the in-process group"};
+      if (c->M != ctxs[0]->M || c->T != ctxs[0]->T || c->S != ctxs[0]->S || c->I != ctxs[0]->I ||
+          c->comm_mode != ctxs[0]->comm_mode)
         throw ConfigError{"smpc_group_init: contexts describe different problems"};
       c->rank = r;
       c->world = n;
@@ -1737,6 +1785,17 @@ smpc_status smpc_comm_unique_id(uint8_t id_out[128]) {
   ncclUniqueId id;
   if (api->GetUniqueId(&id) != 0) return SMPC_ERR_CUDA;
   memcpy(id_out, id.internal, 128);
+  return SMPC_OK;
+}
+
+smpc_status smpc_comm_set_mode(smpc_ctx* c, int32_t mode) {
+  if (!c || (mode != SMPC_COMM_SINGLE && mode != SMPC_COMM_EXACT)) return SMPC_ERR_ARGUMENT;
+  c->comm_mode = mode;
+  fill_args(c);
+  if (c->graph) {
+    cudaGraphExecDestroy(c->graph);
+    c->graph = nullptr;
+  }
   return SMPC_OK;
 }
 

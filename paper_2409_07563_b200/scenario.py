@@ -142,6 +142,11 @@ class SmpcLoopResult(ctypes.Structure):
                 ("mean_solve_ms", ctypes.c_double), ("steps", ctypes.c_int64)]
 
 
+def _lround(x: float) -> int:
+    """std::lround: halves round away from zero (Python's round() is half-even)."""
+    return int(math.floor(x + 0.5)) if x >= 0 else -int(math.floor(-x + 0.5))
+
+
 @dataclasses.dataclass
 class Costmap:
     """Costmap2D (costmap.hpp:17-63): binary grid, row 0 at the lowest y."""
@@ -153,8 +158,8 @@ class Costmap:
 
     @staticmethod
     def empty(width_m: float, height_m: float, resolution: float, origin_x: float, origin_y: float) -> "Costmap":
-        cx = int(round(width_m / resolution))
-        cy = int(round(height_m / resolution))
+        cx = _lround(width_m / resolution)
+        cy = _lround(height_m / resolution)
         return Costmap(np.zeros((cy, cx), np.uint8), resolution, origin_x, origin_y)
 
     def fill_rect(self, x0: float, y0: float, x1: float, y1: float, occupied: bool = True) -> None:
@@ -474,6 +479,15 @@ def autorally_scenario(num_samples: int = 8192, horizon: int = 100, seed: int = 
                     target=[0.0, 0.0, 0.0, 0.0, 4.0, 0.0, 0.0], weights=[0.0, 0.5, 1.0, 0.1, 1.0, 0.1, 0.1],
                     mlp_weights=autorally_mlp_weights(weights_seed), controller=controller,
                     initial_state={"V_X": 2.0})
+
+
+def default_timing_scenario(num_samples: int = 1024, seed: int = 0) -> Scenario:
+    """bench.cpp:178-185, the reference's own timing subject (the paper's
+    protocol): diff-drive + diff_drive_nav on the default
+    all-free 11 m x 11 m map at 0.1 m, ScenarioConfig defaults otherwise
+    (T = 100, dt = 0.02, lambda = 1, sigma = 0.2), starting at (-2, -2)."""
+    return Scenario(num_samples=num_samples, rng_seed=seed, dynamics="diff_drive", cost="diff_drive_nav",
+                    controller="mppi", initial_state={"X": -2.0, "Y": -2.0})
 
 
 def default_sweep_scenario() -> Scenario:

@@ -27,28 +27,38 @@ int main(int argc, char** argv) {
   const int threads = argc > 2 ? std::atoi(argv[2]) : (int)std::thread::hardware_concurrency();
   const bool fma_variant = argc > 3 ? std::atoi(argv[3]) != 0 : true;
   std::atomic<uint64_t> bad_log{0}, bad_sin{0}, bad_cos{0}, checked{0};
+  // fingerprint of the HOST libm over the visited inputs ([fn][top byte of x]),
+  // the value the device-side exhaustive check (smpc_libm_hash) must reproduce
+  std::vector<std::atomic<uint64_t>> hash(3 * 256);
+  for (auto& h : hash) h = 0;
   std::vector<std::thread> pool;
   for (int w = 0; w < threads; ++w) {
     pool.emplace_back([&, w] {
       uint64_t bl = 0, bs = 0, bc = 0, n = 0;
+      std::vector<uint64_t> hl(3 * 256, 0);
       for (uint64_t i = (uint64_t)w * stride; i < (1ULL << 32); i += stride * threads) {
         uint32_t u = (uint32_t)i;
         float x;
         std::memcpy(&x, &u, 4);
-        if (!same(smpc_glibc::logf_glibc(x), logf(x))) {
+        const float lg = logf(x), sn = sinf(x), cs = cosf(x);
+        hl[0 * 256 + (u >> 24)] += smpc_glibc::libm_hash_term(u, lg);
+        hl[1 * 256 + (u >> 24)] += smpc_glibc::libm_hash_term(u, sn);
+        hl[2 * 256 + (u >> 24)] += smpc_glibc::libm_hash_term(u, cs);
+        if (!same(smpc_glibc::logf_glibc(x), lg)) {
           if (bl < 3) std::fprintf(stderr, "logf mismatch %08x\n", u);
           ++bl;
         }
-        if (!same((fma_variant ? smpc_glibc::sinf_glibc<true>(x) : smpc_glibc::sinf_glibc<false>(x)), sinf(x))) {
+        if (!same((fma_variant ? smpc_glibc::sinf_glibc<true>(x) : smpc_glibc::sinf_glibc<false>(x)), sn)) {
           if (bs < 3) std::fprintf(stderr, "sinf mismatch %08x\n", u);
           ++bs;
         }
-        if (!same((fma_variant ? smpc_glibc::cosf_glibc<true>(x) : smpc_glibc::cosf_glibc<false>(x)), cosf(x))) {
+        if (!same((fma_variant ? smpc_glibc::cosf_glibc<true>(x) : smpc_glibc::cosf_glibc<false>(x)), cs)) {
           if (bc < 3) std::fprintf(stderr, "cosf mismatch %08x\n", u);
           ++bc;
         }
         ++n;
       }
+      for (int k = 0; k < 3 * 256; ++k) hash[k] += hl[k];
       bad_log += bl;
       bad_sin += bs;
       bad_cos += bc;
@@ -56,6 +66,12 @@ int main(int argc, char** argv) {
     });
   }
   for (auto& t : pool) t.join();
+  if (const char* hp = std::getenv("SMPC_LIBM_HASH_OUT")) {
+    if (FILE* f = std::fopen(hp, "w")) {
+      for (int k = 0; k < 3 * 256; ++k) std::fprintf(f, "%llu\n", (unsigned long long)hash[k].load());
+      std::fclose(f);
+    }
+  }
   std::printf("{\"checked\": %llu, \"logf_mismatch\": %llu, \"sinf_mismatch\": %llu, \"cosf_mismatch\": %llu}\n",
               (unsigned long long)checked.load(), (unsigned long long)bad_log.load(),
               (unsigned long long)bad_sin.load(), (unsigned long long)bad_cos.load());

@@ -306,13 +306,16 @@ def test_full_size_di_swarm_properties(mods):
     assert close(sol.controls, acc.astype(np.float32))
 
 
+@pytest.mark.parametrize("mode", ["single", "exact"])
 @pytest.mark.parametrize("n", [2, 3, 8])
 @pytest.mark.parametrize("name", ["cartpole", "double_integrator", "unicycle_road"])
-def test_shard_group_matches_single(mods, name, n):
-    """World > 1 device path (gathers + rank-ordered combine) on one GPU:
-    rho/argmin exact, U* within tolerance, every rank bitwise identical."""
+def test_shard_group_matches_single(mods, name, n, mode):
+    """World > 1 device path (gathers + rank-ordered combine) on one GPU, in
+    both exchange modes (one all-gathered record per iteration with the
+    rescaled combine, or the three exact collectives): rho/argmin exact, U*
+    within tolerance, every rank bitwise identical."""
     sc = scenarios(mods["S"])[name]
-    grp = mods["C"].ShardGroup(sc, n)
+    grp = mods["C"].ShardGroup(sc, n, mode=mode)
     ref = mods["OracleController"](sc, "port")
     x0 = sc.x0()
     for solve in range(2):

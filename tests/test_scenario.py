@@ -64,3 +64,11 @@ def test_costmap_text_roundtrip(tmp_path):
     cm.save(path)
     back = S.Costmap.load(path)
     assert np.array_equal(back.grid, cm.grid) and back.resolution == cm.resolution
+
+
+def test_costmap_empty_rounds_halves_away_from_zero():
+    """Costmap2D ctor uses std::lround (costmap.cpp:22-23): 0.25 m at 0.1 m is
+    2.5 cells -> 3 (Python's round() would give 2)."""
+    cm = S.Costmap.empty(0.25, 0.45, 0.1, 0.0, 0.0)  # 2.5 x 4.5 cells
+    assert cm.grid.shape == (5, 3)
+    assert S._lround(2.5) == 3 and S._lround(-2.5) == -3 and S._lround(2.49) == 2
