@@ -67,7 +67,7 @@ METRIC = "rollout samples/s per MPPI iteration (compute_control, I=1)"
 SWEEP = [("cartpole", 2048), ("cartpole", 8192),
          ("quadrotor", 128), ("quadrotor", 1024), ("quadrotor", 8192), ("quadrotor", 16384),
          ("diffdrive", 2000), ("bicycle", 2000),
-         ("autorally", 8192),
+         ("autorally", 8192), ("autorally_rmppi", 8192),
          ("di", 65536), ("di", 262144),
          ("paper", 128), ("paper", 1024), ("paper", 2048), ("paper", 8192), ("paper", 16384)]
 
@@ -88,7 +88,10 @@ def make_scenario(workload: str, n: int) -> S.Scenario:
     if workload == "autorally":
         return S.autorally_scenario(num_samples=n, horizon=100, seed=21, controller="tube")
     if workload == "autorally_rmppi":
-        return S.autorally_scenario(num_samples=n, horizon=100, seed=21, controller="rmppi")
+        sc = S.autorally_scenario(num_samples=n, horizon=100, seed=21, controller="rmppi")
+        sc.feedback_gain = [[0.0, -0.3, -0.5, 0.0, 0.0, -0.2, 0.0], [0.0, 0.0, 0.0, 0.0, -0.4, 0.0, 0.0]]
+        sc.cost_threshold, sc.num_candidates = 5000.0, 9
+        return sc
     raise SystemExit(f"unknown workload {workload}")
 
 
@@ -420,8 +423,8 @@ def run_sweep(args, device, flush, fp32_peak):
             ref = workload in REFERENCE_WORKLOADS
             cpu = {}
             for w in ([1, 0] if ref else [1]):
-                c = cpu_reference_run(sc, steps=5, warmup=1, budget_s=args.sweep_cpu_budget, prefer_ref=ref,
-                                      workers=w)
+                c = cpu_reference_run(sc, steps=5, warmup=1 if ref else 0, budget_s=args.sweep_cpu_budget,
+                                      prefer_ref=ref, workers=w)
                 cpu[f"w{c['cores']}"] = {"ms_per_iter": c["ms"], "samples_per_s": c["value"], "kind": c["kind"],
                                          "solves": c["n"]}
             ent["cpu"] = cpu

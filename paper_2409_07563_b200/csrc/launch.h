@@ -32,6 +32,7 @@ constexpr int kUpdateCtasPerSm = SMPC_UPDATE_MIN_BLOCKS2;  // resident update CT
 #define SMPC_UPDATE_QUADS_PER_UNIT 2
 #endif
 constexpr int kUpdateQuadsPerUnit = SMPC_UPDATE_QUADS_PER_UNIT;  // quads per update work unit
+constexpr int kUpdateSlot = kUpdateQuadsPerUnit * 4;  // per-warp partial: the group's QW*4 entry sums
 // Shards up to this many samples pre-generate the iteration's noise in one
 // parallel pass (gen_zq_kernel) instead of inside each sample's serial chain.
 constexpr long long kZqMaxSamples = 16384;
@@ -207,6 +208,8 @@ struct IterArgs {
   float fb_gain[kMaxNU * kMaxNX];  // K, row-major [NU][NX]
   int n_cand;
   double cost_threshold;
+  double* rm_score;  // [32] candidate scores (warp-cooperative models' select)
+  float* rm_z;       // [32][kMaxNX] candidate states
   // Indexed rollout (export_sample_trajectories re-roll): thread i rolls out
   // global sample sample_idx[i] (nullptr: m_begin + i)
   const long long* sample_idx;

@@ -134,12 +134,15 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
 
 // Shared-memory carve-up (bytes); host and device agree through this struct.
 struct Smem {
-  int w2hi, w2lo, h0, params, sig2, sigma, mean, bar, total;
-  __host__ __device__ Smem(int S, int TU) {
+  int w2hi, w2lo, h0, xs, params, sig2, sigma, mean, bar, total;
+  // RM: both RMPPI systems in one CTA: an A-operand pair per system and the
+  // nominal states exchanged for the real system's feedback
+  __host__ __device__ Smem(int S, int TU, bool RM = false) {
     w2hi = 0;
     w2lo = w2hi + kWBytes;
-    h0 = w2lo + kWBytes;                        // [hi|lo][128 x 32]
-    params = h0 + 2 * kHBytes;                  // W1 b1 b2 W3 b3 (fp32)
+    h0 = w2lo + kWBytes;                        // [sys][hi|lo][128 x 32]
+    xs = h0 + (RM ? 2 : 1) * 2 * kHBytes;       // RM: nominal x_t of each sample [128][8]
+    params = xs + (RM ? kTile * 8 * 4 : 0);     // W1 b1 b2 W3 b3 (fp32)
     sig2 = (params + (TOTAL - HID * HID) * 4 + 15) / 16 * 16;
     sigma = sig2 + TU * 8;
     mean = sigma + TU * 4;
@@ -148,14 +151,22 @@ struct Smem {
   }
 };
 
-template <class Dyn, class Cost, bool INJ, bool IMP>
-__global__ void __launch_bounds__(kTile, 4) mlp_rollout_kernel(const IterArgs a, const Dyn dyn, Cost cost) {
+// RM = RMPPI (a.rmppi, S = 2): one CTA of 256 threads holds both systems of
+// the same 128 samples (threads 0-127 nominal, 128-255 real), two M = 128
+// MMAs per K-step into TMEM columns [0,32) and [32,64), so the real system's
+// sampled control gets u + K (x_real,t - x_nominal,t) of its own sample
+// (states exchanged through shared memory, one extra CTA barrier per step).
+template <class Dyn, class Cost, bool INJ, bool IMP, bool RM>
+__global__ void __launch_bounds__(RM ? 2 * kTile : kTile, RM ? 2 : 4)
+    mlp_rollout_kernel(const IterArgs a, const Dyn dyn, Cost cost) {
   constexpr int NU = 2, NX = 7, NY = 7;
-  const int S = a.S, sys = blockIdx.y;
+  constexpr int NTH = RM ? 2 * kTile : kTile;
+  const int S = a.S;
+  const int sys = RM ? (int)(threadIdx.x >> 7) : (int)blockIdx.y;
   extern __shared__ __align__(1024) unsigned char smem[];
   if (aborted(a)) return;
   const int T = a.T, TU = T * NU;
-  const Smem L(S, TU);
+  const Smem L(S, TU, RM);
   float* prm = reinterpret_cast<float*>(smem + L.params);  // W1T [0,192) b1 [192,224) b2 [224,256) W3T [256,384) b3 [384,388)
   const float* sW1 = prm;
   const float* sB1 = prm + HID * IN;
@@ -168,10 +179,12 @@ __global__ void __launch_bounds__(kTile, 4) mlp_rollout_kernel(const IterArgs a,
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L.bar);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L.bar + 8);
   const int tid = threadIdx.x, warp = tid >> 5;
+  const int row = tid & (kTile - 1);  // sample row of this thread's system tile (= its TMEM lane)
+  float* xs_s = reinterpret_cast<float*>(smem + L.xs);
 
   // ---- one-time staging: W2 as TF32 hi/lo operand tiles, the SIMT layers, sampler tables
   const float* w = dyn.w;
-  for (int e = tid; e < HID * HID; e += kTile) {
+  for (int e = tid; e < HID * HID; e += NTH) {
     const int n = e / HID, k = e % HID;  // W2[n][k]: B operand row n (output unit), K-major
     const float v = __ldg(w + W2 + e);
     const float hi = to_tf32(v);
@@ -179,18 +192,19 @@ __global__ void __launch_bounds__(kTile, 4) mlp_rollout_kernel(const IterArgs a,
     *reinterpret_cast<float*>(smem + L.w2lo + core_off(n, k)) = to_tf32(v - hi);
   }
   // SIMT layers, transposed for packed broadcast reads: W1T[k][j], b1, b2, W3T[j][q], b3
-  for (int e = tid; e < HID * IN; e += kTile) prm[(e % IN) * HID + e / IN] = __ldg(w + W1 + e);
-  for (int e = tid; e < HID; e += kTile) prm[HID * IN + e] = __ldg(w + B1 + e), prm[HID * IN + HID + e] = __ldg(w + B2 + e);
-  for (int e = tid; e < OUT * HID; e += kTile) prm[HID * IN + 2 * HID + (e % HID) * OUT + e / HID] = __ldg(w + W3 + e);
-  for (int e = tid; e < OUT; e += kTile) prm[HID * IN + 2 * HID + OUT * HID + e] = __ldg(w + B3 + e);
-  for (int k = tid; k < TU; k += kTile) {
+  for (int e = tid; e < HID * IN; e += NTH) prm[(e % IN) * HID + e / IN] = __ldg(w + W1 + e);
+  for (int e = tid; e < HID; e += NTH) prm[HID * IN + e] = __ldg(w + B1 + e), prm[HID * IN + HID + e] = __ldg(w + B2 + e);
+  for (int e = tid; e < OUT * HID; e += NTH) prm[HID * IN + 2 * HID + (e % HID) * OUT + e / HID] = __ldg(w + W3 + e);
+  for (int e = tid; e < OUT; e += NTH) prm[HID * IN + 2 * HID + OUT * HID + e] = __ldg(w + B3 + e);
+  for (int k = tid; k < TU; k += NTH) {
     sigma_s[k] = a.sigma[k];
     if (IMP) sig2_s[k] = a.sig2_pow2 ? 1.0 / a.sig2[k] : a.sig2[k];  // exact inverse of a power of two
   }
-  for (int k = tid; k < S * TU; k += kTile) mean_s[k] = a.mean_in[k];
+  for (int k = tid; k < S * TU; k += NTH) mean_s[k] = a.mean_in[k];
+  constexpr int kCols = RM ? 64 : 32;  // fp32 accumulator columns: 32 per system
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "n"(32));
+                 "n"(kCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) mbar_init(bar, 1);
@@ -200,7 +214,7 @@ __global__ void __launch_bounds__(kTile, 4) mlp_rollout_kernel(const IterArgs a,
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
-  const int i = blockIdx.x * kTile + tid;
+  const int i = blockIdx.x * kTile + row;
   const bool active = i < a.M_local;
   const long long m = (a.sample_idx && active) ? a.sample_idx[i] : a.m_begin + i;
   const bool is_mean = a.with_mean && m == 0;
@@ -217,11 +231,30 @@ __global__ void __launch_bounds__(kTile, 4) mlp_rollout_kernel(const IterArgs a,
   const size_t zi = (size_t)(active ? i : 0);
   float4 zn = a.zq ? __ldg(a.zq + zi) : make_float4(0.f, 0.f, 0.f, 0.f);
   uint32_t phase = 0;
-  unsigned char* hhi = smem + L.h0;
+  unsigned char* hhi = smem + L.h0 + (RM ? sys * 2 * kHBytes : 0);
   unsigned char* hlo = hhi + kHBytes;
   const float* mean_sys = mean_s + sys * TU;  // u = mean_s + eps; eps drawn about system 0's mean
 
   for (int t = 0; t < T; ++t) {
+    // ---- RMPPI ancillary feedback on the real system from the nominal state
+    // of the same sample at time t: fb_c = sum_j K[c][j] (x_real,j - x_nom,j)
+    float fb[NU] = {0.0f, 0.0f};
+    if constexpr (RM) {
+      if (sys == 0) {
+#pragma unroll
+        for (int c = 0; c < NX; ++c) xs_s[row * 8 + c] = x[c];
+      }
+      __syncthreads();
+      if (sys == 1) {
+#pragma unroll
+        for (int c = 0; c < NU; ++c) {
+          float acc = 0.0f;
+#pragma unroll
+          for (int j = 0; j < NX; ++j) acc = F_ADD(acc, F_MUL(a.fb_gain[c * NX + j], F_SUB(x[j], xs_s[row * 8 + j])));
+          fb[c] = acc;
+        }
+      }
+    }
     // ---- noise (sampling.cpp:64-88) and the sampled, clamped control
     float u[NU], uc[NU];
 #pragma unroll
@@ -248,6 +281,9 @@ __global__ void __launch_bounds__(kTile, 4) mlp_rollout_kernel(const IterArgs a,
       if constexpr (IMP) {
         const double me = D_MUL((double)mu, (double)e);
         imp = D_ADD(imp, a.sig2_pow2 ? D_MUL(me, sig2_s[k]) : __ddiv_rn(me, sig2_s[k]));
+      }
+      if constexpr (RM) {
+        if (sys == 1) u[c] = F_ADD(u[c], fb[c]);
       }
     }
     dyn.clamp_control(u, uc);
@@ -276,8 +312,8 @@ __global__ void __launch_bounds__(kTile, 4) mlp_rollout_kernel(const IterArgs a,
         hv[jj] = to_tf32(h[jj]);
         lv[jj] = to_tf32(h[jj] - hv[jj]);
       }
-      *reinterpret_cast<float4*>(hhi + core_off(tid, j0)) = make_float4(hv[0], hv[1], hv[2], hv[3]);
-      *reinterpret_cast<float4*>(hlo + core_off(tid, j0)) = make_float4(lv[0], lv[1], lv[2], lv[3]);
+      *reinterpret_cast<float4*>(hhi + core_off(row, j0)) = make_float4(hv[0], hv[1], hv[2], hv[3]);
+      *reinterpret_cast<float4*>(hlo + core_off(row, j0)) = make_float4(lv[0], lv[1], lv[2], lv[3]);
     }
     // ---- layer 2 on the tensor cores: D = H1 W2^T (3xTF32), one issuing thread
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy smem writes -> async proxy
@@ -285,14 +321,18 @@ __global__ void __launch_bounds__(kTile, 4) mlp_rollout_kernel(const IterArgs a,
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     if (tid == 0) {
-      const uint32_t ahi = smem_u32(hhi), alo = ahi + kHBytes;
       const uint32_t bhi = smem_u32(smem + L.w2hi), blo = smem_u32(smem + L.w2lo);
 #pragma unroll
-      for (int kk = 0; kk < HID / 8; ++kk) {  // K-step of 8 TF32 = 2 core-matrix chunks = 256 B
-        const uint32_t off = (uint32_t)kk * 2u * kLBO;
-        mma_tf32(tmem, smem_desc(ahi + off), smem_desc(bhi + off), kk > 0 ? 1u : 0u);
-        mma_tf32(tmem, smem_desc(ahi + off), smem_desc(blo + off), 1u);
-        mma_tf32(tmem, smem_desc(alo + off), smem_desc(bhi + off), 1u);
+      for (int ss = 0; ss < (RM ? 2 : 1); ++ss) {
+        const uint32_t ahi = smem_u32(smem + L.h0 + ss * 2 * kHBytes), alo = ahi + kHBytes;
+        const uint32_t d = tmem + (uint32_t)(ss * 32);  // system ss: accumulator columns [32 ss, 32 ss + 32)
+#pragma unroll
+        for (int kk = 0; kk < HID / 8; ++kk) {  // K-step of 8 TF32 = 2 core-matrix chunks = 256 B
+          const uint32_t off = (uint32_t)kk * 2u * kLBO;
+          mma_tf32(d, smem_desc(ahi + off), smem_desc(bhi + off), kk > 0 ? 1u : 0u);
+          mma_tf32(d, smem_desc(ahi + off), smem_desc(blo + off), 1u);
+          mma_tf32(d, smem_desc(alo + off), smem_desc(bhi + off), 1u);
+        }
       }
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                    : "memory");
@@ -303,7 +343,7 @@ __global__ void __launch_bounds__(kTile, 4) mlp_rollout_kernel(const IterArgs a,
 
     // ---- epilogue: layer 3 + kinematics + Euler + running cost
     float d2[HID];
-    tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16), d2);
+    tmem_ld32(tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(RM ? sys * 32 : 0), d2);
     const ulonglong2 b3v = *reinterpret_cast<const ulonglong2*>(sB3);
     f2 o01 = b3v.x, o23 = b3v.y;
 #pragma unroll
@@ -356,7 +396,7 @@ __global__ void __launch_bounds__(kTile, 4) mlp_rollout_kernel(const IterArgs a,
   __syncthreads();
   if (warp == 0) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(32));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kCols));
   }
   double J = INFINITY;
   if (active) {
@@ -375,26 +415,30 @@ __global__ void __launch_bounds__(kTile, 4) mlp_rollout_kernel(const IterArgs a,
 
   // ---- block (min, argmin) of this system; the last CTA of the whole grid
   // reduces every system (same output as publish_block_min, 2-D grid).
-  {
-    double j = active ? J : INFINITY;
+  // (RM: one pass per system over the whole 256-thread CTA)
+#pragma unroll
+  for (int ss = 0; ss < (RM ? 2 : 1); ++ss) {
+    const bool mine = !RM || sys == ss;
+    double j = active && mine ? J : INFINITY;
     if (!(j == j)) j = INFINITY;
-    long long mm = active ? m : LLONG_MAX;
-    block_argmin<kTile>(j, mm);
+    long long mm = active && mine ? m : LLONG_MAX;
+    block_argmin<NTH>(j, mm);
     if (tid == 0) {
-      a.blk_min[sys * a.n_roll_blocks + blockIdx.x] = j;
-      a.blk_arg[sys * a.n_roll_blocks + blockIdx.x] = mm;
+      const int s_out = RM ? ss : sys;
+      a.blk_min[s_out * a.n_roll_blocks + blockIdx.x] = j;
+      a.blk_arg[s_out * a.n_roll_blocks + blockIdx.x] = mm;
     }
   }
   if (!last_block_done(&a.counters[0], gridDim.x * gridDim.y)) return;
   for (int s = 0; s < S; ++s) {
     double j = INFINITY;
     long long mm = LLONG_MAX;
-    for (int b = tid; b < a.n_roll_blocks; b += kTile) {
+    for (int b = tid; b < a.n_roll_blocks; b += NTH) {
       const double j2 = ((volatile double*)a.blk_min)[s * a.n_roll_blocks + b];
       const long long m2 = ((volatile long long*)a.blk_arg)[s * a.n_roll_blocks + b];
       if (better(j2, m2, j, mm)) j = j2, mm = m2;
     }
-    block_argmin<kTile>(j, mm);
+    block_argmin<NTH>(j, mm);
     if (tid == 0) {
       double* g = a.gather1 + (size_t)a.rank * a.g1s + s * 2;
       g[0] = j;
@@ -403,17 +447,25 @@ __global__ void __launch_bounds__(kTile, 4) mlp_rollout_kernel(const IterArgs a,
   }
 }
 
-template <class Dyn, class Cost>
-cudaError_t launch(const IterArgs& a, const Dyn& dyn, const Cost& cost, cudaStream_t st) {
-  const Smem L(a.S, a.T * 2);
+template <class Dyn, class Cost, bool RM>
+cudaError_t launch_rm(const IterArgs& a, const Dyn& dyn, const Cost& cost, cudaStream_t st) {
+  const Smem L(a.S, a.T * 2, RM);
   const size_t smem = (size_t)L.total;
-  const dim3 grid((unsigned)((a.M_local + kTile - 1) / kTile), (unsigned)a.S), block(kTile);
-  auto k = mlp_rollout_kernel<Dyn, Cost, false, false>;
-  if (a.eps_in) k = a.importance ? mlp_rollout_kernel<Dyn, Cost, true, true> : mlp_rollout_kernel<Dyn, Cost, true, false>;
-  else if (a.importance) k = mlp_rollout_kernel<Dyn, Cost, false, true>;
+  const dim3 grid((unsigned)((a.M_local + kTile - 1) / kTile), RM ? 1u : (unsigned)a.S), block(RM ? 2 * kTile : kTile);
+  auto k = mlp_rollout_kernel<Dyn, Cost, false, false, RM>;
+  if (a.eps_in)
+    k = a.importance ? mlp_rollout_kernel<Dyn, Cost, true, true, RM> : mlp_rollout_kernel<Dyn, Cost, true, false, RM>;
+  else if (a.importance)
+    k = mlp_rollout_kernel<Dyn, Cost, false, true, RM>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k<<<grid, block, smem, st>>>(a, dyn, cost);
   return cudaGetLastError();
+}
+
+template <class Dyn, class Cost>
+cudaError_t launch(const IterArgs& a, const Dyn& dyn, const Cost& cost, cudaStream_t st) {
+  if (a.rmppi && a.S == 2) return launch_rm<Dyn, Cost, true>(a, dyn, cost, st);
+  return launch_rm<Dyn, Cost, false>(a, dyn, cost, st);
 }
 
 template <class Dyn>
@@ -447,6 +499,14 @@ cudaError_t mlp_plant(const IterArgs& a, int ck, const PlantStepArgs& p, cudaStr
   return cudaErrorInvalidValue;
 }
 template <bool F>
+cudaError_t mlp_rmppi(const IterArgs& a, int ck, cudaStream_t st) {
+  switch (ck) {
+    case 0: return launch_rmppi_select_coop_t(a, mlp_make<F>(a.dyn), make_road(a.cost), st);
+    case 3: return launch_rmppi_select_coop_t(a, mlp_make<F>(a.dyn), make_quad<7>(a.cost), st);
+  }
+  return cudaErrorInvalidValue;
+}
+template <bool F>
 cudaError_t mlp_update(const IterArgs& a, cudaStream_t st) {
   return launch_update_t(a, mlp_make<F>(a.dyn), st);
 }
@@ -461,10 +521,10 @@ cudaError_t mlp_generate(const IterArgs& a, float* e, uint8_t* f, cudaStream_t s
 
 ModelOps ops_mlp(bool fma_libm) {
   if (fma_libm)
-    return ModelOps{mlp_rollout<true>, nullptr, mlp_plant<true>, launch_weights, mlp_update<true>, mlp_combine<true>,
-                    mlp_generate, 7, 2, 7};
-  return ModelOps{mlp_rollout<false>, nullptr, mlp_plant<false>, launch_weights, mlp_update<false>, mlp_combine<false>,
-                  mlp_generate, 7, 2, 7};
+    return ModelOps{mlp_rollout<true>, mlp_rmppi<true>, mlp_plant<true>, launch_weights, mlp_update<true>,
+                    mlp_combine<true>, mlp_generate, 7, 2, 7};
+  return ModelOps{mlp_rollout<false>, mlp_rmppi<false>, mlp_plant<false>, launch_weights, mlp_update<false>,
+                  mlp_combine<false>, mlp_generate, 7, 2, 7};
 }
 
 }  // namespace smpc_dev

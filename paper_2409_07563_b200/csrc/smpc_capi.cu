@@ -156,6 +156,8 @@ struct smpc_ctx {
   int rank = 0, world = 1;
   int comm_mode = SMPC_COMM_SINGLE;  // one all-gather per iteration (smpc_comm_set_mode)
   double* d_gather_rec = nullptr;    // [8][rec] packed per-rank records of the single-collective mode
+  double* d_rm_score = nullptr;      // RMPPI candidate scratch (warp-cooperative models)
+  float* d_rm_z = nullptr;
   // host state
   uint64_t solve_count = 0;
   std::string err;
@@ -386,6 +388,8 @@ void fill_args(smpc_ctx* c) {
   for (size_t k = 0; k < c->fb_gain.size(); ++k) a.fb_gain[k] = c->fb_gain[k];
   a.n_cand = p.num_candidates;
   a.cost_threshold = p.cost_threshold;
+  a.rm_score = c->d_rm_score;
+  a.rm_z = c->d_rm_z;
   a.world = c->world;
   a.rank = c->rank;
   a.solve_count = &c->header()->solve_count;
@@ -897,7 +901,7 @@ smpc_status smpc_create(const smpc_problem* problem, smpc_ctx** out) {
       const long long Q = (TU + 3) / 4, QG = (Q + kUpdateQuadsPerUnit - 1) / kUpdateQuadsPerUnit;
       // warps covering one quad group: <= 2 * warps / QG + 2 (each owns >= U / (2 W) units)
       c->upd_slots = (int)(2 * ((warps + QG - 1) / QG) + 3);
-      c->d_blk_part = dalloc<double>((size_t)c->S * QG * c->upd_slots * kUpdateQuadsPerUnit * 4);
+      c->d_blk_part = dalloc<double>((size_t)c->S * QG * c->upd_slots * kUpdateSlot);
     }
     c->d_counters = dalloc<unsigned int>(16);
     c->d_select = dalloc<SelectState>(1);
@@ -915,6 +919,8 @@ smpc_status smpc_create(const smpc_problem* problem, smpc_ctx** out) {
     c->d_gather2 = dalloc<double>((size_t)c->S * 2 * 8);
     c->d_gather3 = dalloc<double>((size_t)c->S * TU * 8);
     c->d_gather_rec = dalloc<double>((size_t)gather_record(c) * 8);
+    c->d_rm_score = dalloc<double>(32);
+    c->d_rm_z = dalloc<float>(32 * kMaxNX);
     // result region: header | controls | states | outputs
     size_t off = align_up(sizeof(ResultHeader), 256);
     c->off_controls = off;
@@ -1018,7 +1024,7 @@ void smpc_destroy(smpc_ctx* c) {
                   c->d_gather3, c->d_blk_arg, c->d_blk_nz, c->d_counters, c->d_costmap, c->d_result,
                   c->d_ro_x0, c->d_ro_mean, c->d_eps, c->d_outputs, c->d_wscratch, c->d_flags,
                   c->d_cand, c->d_cand_e, c->d_cand_cnt, c->d_cand_off, c->d_select, c->d_eq_cnt, c->d_eq_off,
-                  c->d_dyn_tensor, c->d_zq};
+                  c->d_dyn_tensor, c->d_zq, c->d_gather_rec, c->d_rm_score, c->d_rm_z};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->h_result) cudaFreeHost(c->h_result);

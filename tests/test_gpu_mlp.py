@@ -99,6 +99,37 @@ def test_mlp_compute_control_matches_oracle(mods, controller):
             gpu.set_mean(b["controls"])
 
 
+@pytest.mark.parametrize("threshold", [float("inf"), -1.0])
+def test_mlp_rmppi_matches_oracle(mods, threshold):
+    """RMPPI on the tcgen05 MLP rollout (BASELINE.json configs[3] as stated:
+    "... with Tube-MPPI / RMPPI dual rollouts"): both systems of a sample in
+    one CTA, the real system's control gets u + K (x_real - x_nominal) of the
+    same sample, one control sequence from the real costs, and the nominal
+    state chosen by the warp-cooperative candidate scoring. Thresholds away
+    from any candidate's cost (all admissible / none admissible) keep the
+    discrete choice independent of the tolerance-level MLP differences."""
+    S = mods["S"]
+    sc = S.autorally_scenario(num_samples=2048, horizon=100, seed=21, controller="rmppi")
+    sc.feedback_gain = [[0.0, -0.3, -0.5, 0.0, 0.0, -0.2, 0.0], [0.0, 0.0, 0.0, 0.0, -0.4, 0.0, 0.0]]
+    sc.cost_threshold = threshold
+    sc.num_candidates = 7
+    gpu = mods["C"].make_controller(sc)
+    ref = mods["OracleController"](sc, "port")
+    x = sc.x0()
+    rng = np.random.default_rng(3)
+    for solve in range(3):
+        a = gpu.tube_compute_control(x)
+        b = ref.rmppi_compute_control(x)
+        assert close(a.nominal_state, b["nominal_state"]), solve
+        assert close(a.real.weights.baseline, b["baseline"]), (solve, a.real.weights.baseline, b["baseline"])
+        assert np.array_equal(a.nominal.controls, a.real.controls)  # one control sequence
+        print("rmppi U* rel err", relerr(a.nominal.controls, b["controls"]), "choice", b["choice"])
+        assert close(a.nominal.controls, b["controls"])
+        assert close(a.nominal.states, b["nominal_states"]) and close(a.real.states, b["real_states"])
+        gpu.set_mean(b["controls"])
+        x = (b["nominal_states"][1] + rng.standard_normal(x.size).astype(np.float32) * 0.05).astype(np.float32)
+
+
 def test_mlp_large_batch_properties(mods):
     """N = 65536 (every SM busy, several CTAs per SM): weights sum to one,
     argmin consistent with a strided oracle check of the device costs."""
