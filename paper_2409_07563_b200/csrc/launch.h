@@ -164,6 +164,10 @@ struct IterArgs {
   const float* eps_in;   // injected [M_local][T][NU] or nullptr
   const float* tail;     // Phi^-1 tail table
   unsigned long long tail_tex;  // the same table as a 1-D texture object (index-addressed fetch)
+  // normal_icdf over the sampler's whole domain (2^23 floats, 32 MB, built
+  // once per device with the same device arithmetic as the in-register
+  // path): a texture object, or 0
+  unsigned long long full_tex;
   // rollout outputs
   double* costs;   // [S][M_local]
   float* outputs;  // [S][M_local][T][NY] or nullptr

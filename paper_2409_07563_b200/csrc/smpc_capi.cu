@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <mutex>
 #include <cstdio>
 #include <string>
 #include <vector>
@@ -116,6 +117,7 @@ struct smpc_ctx {
   int *d_cand = nullptr, *d_cand_cnt = nullptr;
   double* d_cand_e = nullptr;
   unsigned long long tail_tex = 0;
+  unsigned long long full_tex = 0;  // per-device full-domain normal_icdf table (shared, never freed)
   int upd_slots = 4;
   long long* d_cand_off = nullptr;
   long long *d_blk_arg = nullptr, *d_blk_nz = nullptr;
@@ -350,6 +352,39 @@ uint32_t tail_table_size(uint32_t* j_lo_out, uint32_t* j_hi_out);
 
 int gather_record(const smpc_ctx* c) { return 4 * c->S + c->S * c->T * c->nu; }
 
+// normal_icdf over the sampler's whole 2^23-point domain, one 32 MB table per
+// device shared by every context (it depends on nothing but the arithmetic),
+// built by the same icdf_quad_words path the kernels evaluate in registers.
+struct FullIcdfTable {
+  float* d = nullptr;
+  unsigned long long tex = 0;
+};
+std::mutex g_full_mu;
+FullIcdfTable g_full[64];
+
+unsigned long long full_icdf_table(const IterArgs& base, int device, cudaStream_t st) {
+  std::lock_guard<std::mutex> lk(g_full_mu);
+  FullIcdfTable& t = g_full[device & 63];
+  if (!t.tex) {
+    float* d = nullptr;
+    CK(cudaMalloc(&d, sizeof(float) << 23));
+    CK(launch_icdf_domain(base, d, st));
+    CK(cudaStreamSynchronize(st));
+    cudaResourceDesc rd = {};
+    rd.resType = cudaResourceTypeLinear;
+    rd.res.linear.devPtr = d;
+    rd.res.linear.desc = cudaCreateChannelDesc<float>();
+    rd.res.linear.sizeInBytes = sizeof(float) << 23;
+    cudaTextureDesc td = {};
+    td.readMode = cudaReadModeElementType;
+    cudaTextureObject_t tex = 0;
+    CK(cudaCreateTextureObject(&tex, &rd, &td, nullptr));
+    t.d = d;
+    t.tex = (unsigned long long)tex;
+  }
+  return t.tex;
+}
+
 void fill_args(smpc_ctx* c) {
   IterArgs& a = c->base;
   const smpc_problem& p = c->p;
@@ -406,6 +441,7 @@ void fill_args(smpc_ctx* c) {
   a.zq = nullptr;
   a.tail = c->d_tail;
   a.tail_tex = c->tail_tex;
+  a.full_tex = c->full_tex;
   a.costs = c->d_costs;
   a.outputs = nullptr;
   a.n_roll_blocks = c->n_roll_blocks;
@@ -1001,6 +1037,8 @@ smpc_status smpc_create(const smpc_problem* problem, smpc_ctx** out) {
       c->ev.push_back(e);
     }
     fill_args(c);
+    c->full_tex = full_icdf_table(c->base, p.device, c->stream);
+    c->base.full_tex = c->full_tex;
     CK(cudaStreamSynchronize(c->stream));
   });
   if (st != SMPC_OK) {
@@ -1547,6 +1585,20 @@ int32_t smpc_kernels_per_solve(const smpc_ctx* c) {
   const int rm = c->p.controller_kind == SMPC_CTRL_RMPPI ? 1 : 0;
   if (c->p.controller_kind == SMPC_CTRL_CEM) return 2 + c->I * (1 + 11 + 1 + zq);  // rollout, select (init+8+2), update
   return 2 + rm + c->I * (3 + zq + (c->world > 1 ? 1 : 0));
+}
+
+smpc_status smpc_icdf_table(smpc_ctx* c, float* out) {
+  if (!c || !out) return SMPC_ERR_ARGUMENT;
+  return guarded(c, [&] {
+    const float* d;
+    {
+      std::lock_guard<std::mutex> lk(g_full_mu);
+      d = g_full[c->p.device & 63].d;
+    }
+    if (!d) throw RuntimeError{"icdf table not built"};
+    CK(cudaMemcpyAsync(out, d, sizeof(float) << 23, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  });
 }
 
 smpc_status smpc_icdf_domain(smpc_ctx* c, float* out) {

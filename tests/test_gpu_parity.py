@@ -84,6 +84,18 @@ def test_icdf_whole_domain_bit_exact(mods):
     assert bad.size == 0, (bad[:10], out[bad[:10]], ref[bad[:10]])
 
 
+def test_full_domain_icdf_table_bit_exact(mods):
+    """The resident full-domain normal_icdf table the steady-state rollout
+    reads for part of its draws equals the in-register evaluation (and so the
+    oracle) on all 2^23 uniforms."""
+    O = mods["Oracle"]("port")
+    ref = O.icdf_domain()
+    eng = mods["C"].RolloutEngine(mods["S"].cartpole_scenario(num_samples=16, horizon=4))
+    out = np.zeros(1 << 23, np.float32)
+    eng._check(eng.lib.smpc_icdf_table(eng.ctx, out))
+    assert np.array_equal(out.view(np.uint32), ref.view(np.uint32))
+
+
 def test_branch_free_sqrt_exhaustive(mods):
     """The cost / dynamics functors' branch-free sqrt (std::sqrt of
     costs.cpp:59, the quaternion norm) equals sqrt.rn.f32 on all 2^32 floats."""
