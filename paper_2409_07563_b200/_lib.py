@@ -25,7 +25,7 @@ EXPORTED = [
     "smpc_launch_iteration", "smpc_synchronize", "smpc_stream", "smpc_kernels_per_solve",
     "smpc_rollout_kernel_ms", "smpc_icdf_domain", "smpc_icdf_table", "smpc_comm_unique_id", "smpc_comm_init", "smpc_comm_set_mode", "smpc_group_init",
     "smpc_group_compute_control", "smpc_host_libm_uses_fma",
-    "smpc_measure_fp32_peak", "smpc_sqrt_check", "smpc_libm_hash", "smpc_select_noise_strategy", "smpc_noise_strategy_rule",
+    "smpc_measure_fp32_peak", "smpc_sqrt_check", "smpc_libm_hash", "smpc_fast_math_check", "smpc_select_noise_strategy", "smpc_noise_strategy_rule",
     "smpc_version",
 ]
 
@@ -120,6 +120,8 @@ def load(path: str = None) -> ctypes.CDLL:
     L.smpc_sqrt_check.restype = ctypes.c_int
     L.smpc_libm_hash.argtypes = [ctypes.c_int32, ctypes.c_int32, P(ctypes.c_uint64)]
     L.smpc_libm_hash.restype = ctypes.c_int
+    L.smpc_fast_math_check.argtypes = [ctypes.c_int32, ctypes.c_int32, P(ctypes.c_uint64)]
+    L.smpc_fast_math_check.restype = ctypes.c_int
     L.smpc_select_noise_strategy.argtypes = [c_ctx, ctypes.c_int32, ctypes.c_int32, ctypes.c_double, f32p,
                                              P(SmpcNoiseChoice)]
     L.smpc_select_noise_strategy.restype = ctypes.c_int

@@ -300,6 +300,31 @@ GM_HD void sincosf_glibc(float y, float* sp, float* cp) {
   *sp = *cp = u2f(0x7fc00000u);
 }
 
+#if defined(__CUDACC__)
+// sincosf_glibc without a branch for |x| < 120 (the rollout's unchecked
+// loop): the |x| < pi/4 path is the reduce_fast path with n = 0 (x - 0*hpi ==
+// x, sign[0] == 1, table 0: the same operations), the |x| < 2^-12 early
+// returns are selects, and |x| >= 120, inf and NaN give NaN (the sample is
+// then replayed with the exact sincosf_glibc). Equal to sincosf_glibc on every
+// |x| < 120 (exhaustive: smpc_libm_fast_check).
+template <bool FMA>
+__device__ __forceinline__ void sincosf_glibc_fast(float y, float* sp, float* cp) {
+  int n;
+  const double x = reduce_fast<FMA>((double)y, &GM_SINCOSF_TAB[0], &n);
+  const SincosfTable* p = &GM_SINCOSF_TAB[(n >> 1) & 1];
+  const double xs = GM_DMUL(x, GM_SINCOSF_TAB[0].sign[n & 3]), xx = GM_DMUL(x, x);
+  float sv = sinf_poly<FMA>(xs, xx, p, n);
+  float cv = sinf_poly<FMA>(xs, xx, p, n ^ 1);
+  const uint32_t top = abstop12(y);
+  const bool tiny = top < abstop12(0x1p-12f);
+  sv = tiny ? y : sv;
+  cv = tiny ? 1.0f : cv;
+  const bool ok = top < abstop12(120.0f);
+  *sp = ok ? sv : u2f(0x7fc00000u);
+  *cp = ok ? cv : u2f(0x7fc00000u);
+}
+#endif
+
 // Order-independent fingerprint of a function over all 2^32 float inputs
 // (test infrastructure: the device result is compared with the same sum over
 // the host libm, tests/golden/libm_hash.json). NaN outputs hash as the

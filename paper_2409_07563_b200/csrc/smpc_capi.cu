@@ -81,12 +81,17 @@ struct CudaError {
     if (e_ != cudaSuccess) throw CudaError{std::string(#call) + ": " + cudaGetErrorString(e_)}; \
   } while (0)
 
+// Zeroed device buffer. cudaMemset runs on the legacy default stream, which
+// does NOT order with the contexts' non-blocking streams, so the fill is
+// waited for here (allocation paths are cold): kernels rely on zeroed
+// arrival counters and scratch.
 template <typename T>
 T* dalloc(size_t n) {
   if (n == 0) n = 1;
   void* p = nullptr;
   CK(cudaMalloc(&p, n * sizeof(T)));
   CK(cudaMemset(p, 0, n * sizeof(T)));
+  CK(cudaStreamSynchronize(nullptr));
   return static_cast<T*>(p);
 }
 

@@ -39,3 +39,19 @@ def test_device_libm_ports_exhaustive(lib, variant):
     for r, name in enumerate(ROWS):
         bad = np.nonzero(out[r] != want[r])[0]
         assert bad.size == 0, f"{name}: input top bytes {[hex(b) for b in bad[:8]]} differ from the host libm"
+
+
+@pytest.mark.parametrize("variant", ["fma", "generic"])
+def test_fast_math_matches_exact(lib, variant):
+    """The unchecked rollout loop's branch-free math: sincosf (all 2^32
+    floats, |x| < 120 equal to the exact port, NaN beyond -> exact replay),
+    wrap_angle (all 2^32), float division (2^32 random pairs) and the
+    importance term's double division with a precomputed divisor reciprocal
+    (2^31 random pairs) equal the exact device ops wherever they do not
+    return NaN."""
+    out = np.zeros(16, np.uint64)
+    rc = lib.smpc_fast_math_check(0, 1 if variant == "fma" else 0, out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)))
+    assert rc == 0
+    print("fast-path pairs: div", out[4], "ddiv", out[5], "first mismatches", [hex(int(v)) for v in out[6:]])
+    assert out[0] == 0 and out[1] == 0 and out[2] == 0 and out[3] == 0, out
+    assert out[4] > (1 << 29) and out[5] > (1 << 28)
