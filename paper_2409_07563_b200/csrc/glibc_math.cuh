@@ -300,21 +300,45 @@ GM_HD void sincosf_glibc(float y, float* sp, float* cp) {
   *sp = *cp = u2f(0x7fc00000u);
 }
 
-#if defined(__CUDACC__)
 // sincosf_glibc without a branch for |x| < 120 (the rollout's unchecked
 // loop): the |x| < pi/4 path is the reduce_fast path with n = 0 (x - 0*hpi ==
 // x, sign[0] == 1, table 0: the same operations), the |x| < 2^-12 early
 // returns are selects, and |x| >= 120, inf and NaN give NaN (the sample is
-// then replayed with the exact sincosf_glibc). Equal to sincosf_glibc on every
-// |x| < 120 (exhaustive: smpc_libm_fast_check).
+// then replayed with the exact sincosf_glibc). No constant-bank table reads:
+// __sincosf_table[1] is table 0 with every cosine coefficient negated and the
+// same sine coefficients, so its cosine polynomial is the exact negation of
+// table 0's (round-to-nearest is symmetric; the cosine polynomial is >= 0.7,
+// never an exact zero), and sign[n & 3] = {1,-1,-1,1} is a conditional
+// negation. Equal to sincosf_glibc on every |x| < 120 (exhaustive:
+// smpc_fast_math_check).
 template <bool FMA>
-__device__ __forceinline__ void sincosf_glibc_fast(float y, float* sp, float* cp) {
-  int n;
-  const double x = reduce_fast<FMA>((double)y, &GM_SINCOSF_TAB[0], &n);
-  const SincosfTable* p = &GM_SINCOSF_TAB[(n >> 1) & 1];
-  const double xs = GM_DMUL(x, GM_SINCOSF_TAB[0].sign[n & 3]), xx = GM_DMUL(x, x);
-  float sv = sinf_poly<FMA>(xs, xx, p, n);
-  float cv = sinf_poly<FMA>(xs, xx, p, n ^ 1);
+GM_HD void sincosf_glibc_fast(float y, float* sp, float* cp) {
+  constexpr double hpi_inv = 0x1.45f306dc9c883p+23, hpi = 0x1.921fb54442d18p+0;
+  constexpr double c0 = 0x1p+0, c1 = -0x1.ffffffd0c621cp-2, c2 = 0x1.55553e1068f19p-5, c3 = -0x1.6c087e89a359dp-10,
+                   c4 = 0x1.99343027bf8c3p-16;
+  constexpr double s1 = -0x1.555545995a603p-3, s2 = 0x1.1107605230bc4p-7, s3 = -0x1.994eb3774cf24p-13;
+  const double xd = (double)y;
+  const double r = GM_DMUL(xd, hpi_inv);
+  const int n = ((int32_t)r + 0x800000) >> 24;
+  const double x = FMA ? GM_DFMA(-(double)n, hpi, xd) : GM_DSUB(xd, GM_DMUL((double)n, hpi));
+  const double xs = ((n + 1) & 2) ? -x : x;  // x * sign[n & 3]
+  const double x2 = GM_DMUL(x, x);
+  // sine polynomial (sinf_poly, n even): table-independent
+  const double x3 = GM_DMUL(xs, x2);
+  const double sa = GM_MADD(FMA, s2, x2, s3);
+  const double x7 = GM_DMUL(x3, x2);
+  const double sb = GM_MADD(FMA, xs, x3, s1);
+  const float S = (float)GM_MADD(FMA, sb, x7, sa);
+  // cosine polynomial (sinf_poly, n odd) with table 0, negated for table 1
+  const double x4 = GM_DMUL(x2, x2);
+  const double ca = GM_MADD(FMA, c3, x2, c4);
+  const double cb = GM_MADD(FMA, c0, x2, c1);
+  const double x6 = GM_DMUL(x4, x2);
+  const double cc = GM_MADD(FMA, cb, x4, c2);
+  const float C0 = (float)GM_MADD(FMA, cc, x6, ca);
+  const float C = (n & 2) ? -C0 : C0;
+  float sv = (n & 1) ? C : S;
+  float cv = (n & 1) ? S : C;
   const uint32_t top = abstop12(y);
   const bool tiny = top < abstop12(0x1p-12f);
   sv = tiny ? y : sv;
@@ -323,7 +347,6 @@ __device__ __forceinline__ void sincosf_glibc_fast(float y, float* sp, float* cp
   *sp = ok ? sv : u2f(0x7fc00000u);
   *cp = ok ? cv : u2f(0x7fc00000u);
 }
-#endif
 
 // Order-independent fingerprint of a function over all 2^32 float inputs
 // (test infrastructure: the device result is compared with the same sum over

@@ -32,6 +32,15 @@ constexpr int kUpdateCtasPerSm = SMPC_UPDATE_MIN_BLOCKS2;  // resident update CT
 #define SMPC_UPDATE_QUADS_PER_UNIT 2
 #endif
 constexpr int kUpdateQuadsPerUnit = SMPC_UPDATE_QUADS_PER_UNIT;  // quads per update work unit
+constexpr size_t kFinishStageMaxBytes = 200 * 1024;
+// Split small-N rollout: samples per cost CTA, so that its per-(sample, t)
+// costs and importance terms stay within 96 KB of shared memory.
+__host__ __device__ inline int split_samples_per_cta(int T, int NU, bool imp) {
+  int sb = 32;
+  const long long per = (long long)T * (1 + (imp ? NU : 0)) * 8;
+  while (sb > 1 && per * sb > 96 * 1024) sb >>= 1;
+  return sb;
+}
 constexpr int kUpdateSlot = kUpdateQuadsPerUnit * 4;  // per-warp partial: the group's QW*4 entry sums
 // Shards up to this many samples pre-generate the iteration's noise in one
 // parallel pass (gen_zq_kernel) instead of inside each sample's serial chain.
@@ -195,6 +204,17 @@ struct IterArgs {
   // single-collective mode (one ncclAllGather per iteration)
   int g1s, g2s, g3s;
   int comm_single;        // single-collective mode: local baselines + rescaled combine
+  int finish_staged;      // finish_solution's states fit the update kernel's shared staging (set at launch)
+  // Split small-N rollout (the reference's split strategy, engine.cpp:130-209):
+  // the rollout kernel runs only the dynamics chain and stores the outputs
+  // (and controls) [S][T][NY|NU][M_local] (sample-minor); a parallel cost
+  // kernel evaluates the running costs / importance terms over (sample, t)
+  // and sums them in the reference's order. A sample whose fast chain flags
+  // is replayed exactly by the rollout kernel (rflag[i] = 1, its J written).
+  int split;
+  float* ytraj;
+  float* utraj;
+  unsigned char* rflag;
   // results
   ResultHeader* header;
   float* controls;  // [S][T][NU]

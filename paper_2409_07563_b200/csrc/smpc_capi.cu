@@ -130,6 +130,12 @@ struct smpc_ctx {
   uint8_t* d_costmap = nullptr;
   float* d_dyn_tensor = nullptr;
   float4* d_zq = nullptr;  // small-N mode noise buffer [Q][M_local]
+  // split small-N rollout (dynamics chain + parallel exact costs): samples per
+  // cost CTA (0 = off), trajectories [S][T][NY|NU][M_local], replay flags
+  int split_sb = 0;
+  long long blk_cap = 0;  // entries of d_blk_min / d_blk_arg
+  float *d_ytraj = nullptr, *d_utraj = nullptr;
+  unsigned char* d_rflag = nullptr;
   bool use_zq = false;     // noise strategy: split (d_zq pass) vs fused (in-register)
   smpc_noise_choice noise_choice = {SMPC_NOISE_AUTO, 0.0, 0.0, 0};
   bool noise_resolved = false;  // set by smpc_select_noise_strategy (default: split iff M_local <= 16384)
@@ -430,6 +436,10 @@ void fill_args(smpc_ctx* c) {
   a.cost_threshold = p.cost_threshold;
   a.rm_score = c->d_rm_score;
   a.rm_z = c->d_rm_z;
+  a.split = 0;  // enabled per launch with the split-noise buffer (enqueue_solve)
+  a.ytraj = c->d_ytraj;
+  a.utraj = c->d_utraj;
+  a.rflag = c->d_rflag;
   a.world = c->world;
   a.rank = c->rank;
   a.solve_count = &c->header()->solve_count;
@@ -610,6 +620,7 @@ void enqueue_solve(smpc_ctx* c, bool timed) {
     if (timed) CK(cudaEventRecord(c->ev[2 * it], c->stream));
     if (c->use_zq) {  // split noise: one parallel pass, off the per-sample serial chain
       a.zq = c->d_zq;
+      a.split = c->d_ytraj ? c->split_sb : 0;  // and the split dynamics / cost rollout
       CK(launch_gen_zq(a, c->nu, c->d_zq, c->stream));
     }
     CK(c->ops.rollout(a, c->p.cost_kind, c->stream));
@@ -721,7 +732,31 @@ void build_graph(smpc_ctx* c) {
   cudaGraphDestroy(g);
 }
 
+// Buffers of the split small-N rollout (when the model runs on the SIMT rollout).
+void alloc_split(smpc_ctx* c, bool refill) {
+  if (c->d_ytraj || c->p.dynamics_kind == SMPC_DYN_MLP) return;
+  // A/B knob (default off: measured slower than the fused chain, whose cost
+  // work the scheduler already overlaps with the dynamics chain)
+  const char* e = getenv("SMPC_SPLIT");
+  if (!e || atoi(e) == 0) return;
+  c->d_ytraj = dalloc<float>((size_t)c->S * c->T * c->ny * c->M_local);
+  c->d_utraj = dalloc<float>((size_t)c->S * c->T * c->nu * c->M_local);
+  c->d_rflag = dalloc<unsigned char>((size_t)c->M_local);
+  c->split_sb = split_samples_per_cta(c->T, c->nu, true);
+  // the cost kernel publishes one block minimum per SB samples
+  const long long need = (long long)c->S * ((c->M_local + c->split_sb - 1) / c->split_sb);
+  if (need > c->blk_cap) {
+    if (c->d_blk_min) cudaFree(c->d_blk_min);
+    if (c->d_blk_arg) cudaFree(c->d_blk_arg);
+    c->d_blk_min = dalloc<double>((size_t)need);
+    c->d_blk_arg = dalloc<long long>((size_t)need);
+    c->blk_cap = need;
+  }
+  if (refill) fill_args(c);
+}
+
 void set_noise(smpc_ctx* c, bool split) {
+  if (split) alloc_split(c, true);
   if (split && !c->d_zq) c->d_zq = dalloc<float4>((size_t)((c->T * c->nu + 3) / 4) * c->M_local);
   if (c->use_zq != split) {
     c->use_zq = split;
@@ -741,7 +776,10 @@ double time_iteration_median(smpc_ctx* c, bool split, int n) {
   IterArgs a = c->base;
   a.do_finish = 0;
   a.iter = 0;
-  if (split) a.zq = c->d_zq;
+  if (split) {
+    a.zq = c->d_zq;
+    a.split = c->d_ytraj ? c->split_sb : 0;
+  }
   float* scratch = nullptr;
   CK(cudaMalloc(&scratch, sizeof(float) * (size_t)c->S * c->T * c->nu));
   a.mean_out = scratch;
@@ -919,7 +957,12 @@ smpc_status smpc_create(const smpc_problem* problem, smpc_ctx** out) {
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p.device);
       int per_sm = kUpdateCtasPerSm;
       if (const char* e = getenv("SMPC_UPDATE_CTAS_PER_SM")) per_sm = std::max(1, atoi(e));  // A/B knob
-      c->n_u_blocks = (int)std::max<long long>(1, std::min<long long>((c->M_local + 255) / 256, (long long)sms * per_sm));
+      // enough warps for one work unit (quad group x 32 candidates) each when
+      // every sample is a candidate, capped at one resident wave
+      const long long QG = ((TU + 3) / 4 + kUpdateQuadsPerUnit - 1) / kUpdateQuadsPerUnit;
+      const long long units = (c->M_local + 31) / 32 * QG;
+      c->n_u_blocks = (int)std::max<long long>(1, std::min<long long>((units + kUpdateWarps - 1) / kUpdateWarps,
+                                                                     (long long)sms * per_sm));
     }
 
     c->d_mean = dalloc<float>((size_t)c->S * TU);
@@ -929,8 +972,9 @@ smpc_status smpc_create(const smpc_problem* problem, smpc_ctx** out) {
     c->d_gamma = dalloc<double>(c->T);
     c->d_costs = dalloc<double>((size_t)c->S * c->M_local);
     c->d_weights = dalloc<double>((size_t)c->S * c->M_local);
-    c->d_blk_min = dalloc<double>((size_t)c->S * c->n_roll_blocks);
-    c->d_blk_arg = dalloc<long long>((size_t)c->S * c->n_roll_blocks);
+    c->blk_cap = (long long)c->S * c->n_roll_blocks;
+    c->d_blk_min = dalloc<double>((size_t)c->blk_cap);
+    c->d_blk_arg = dalloc<long long>((size_t)c->blk_cap);
     c->d_blk_eta = dalloc<double>((size_t)c->S * c->n_w_blocks);
     c->d_blk_nz = dalloc<long long>((size_t)c->S * c->n_w_blocks);
     c->d_cand = dalloc<int>((size_t)c->S * c->M_local);
@@ -952,6 +996,7 @@ smpc_status smpc_create(const smpc_problem* problem, smpc_ctx** out) {
       if (c->M_local <= zq_max) {
         c->d_zq = dalloc<float4>((size_t)((TU + 3) / 4) * c->M_local);
         c->use_zq = true;
+        alloc_split(c, false);
       }
     }
     c->d_eq_cnt = dalloc<int>(c->n_w_blocks);
@@ -1067,7 +1112,8 @@ void smpc_destroy(smpc_ctx* c) {
                   c->d_gather3, c->d_blk_arg, c->d_blk_nz, c->d_counters, c->d_costmap, c->d_result,
                   c->d_ro_x0, c->d_ro_mean, c->d_eps, c->d_outputs, c->d_wscratch, c->d_flags,
                   c->d_cand, c->d_cand_e, c->d_cand_cnt, c->d_cand_off, c->d_select, c->d_eq_cnt, c->d_eq_off,
-                  c->d_dyn_tensor, c->d_zq, c->d_gather_rec, c->d_rm_score, c->d_rm_z};
+                  c->d_dyn_tensor, c->d_zq, c->d_gather_rec, c->d_rm_score, c->d_rm_z,
+                  c->d_ytraj, c->d_utraj, c->d_rflag};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->h_result) cudaFreeHost(c->h_result);
