@@ -23,7 +23,7 @@ EXPORTED = [
     "smpc_shift_control_sequence", "smpc_get_solve_count", "smpc_set_solve_count",
     "smpc_generate_samples", "smpc_rollout", "smpc_compute_weights", "smpc_sorted_samples", "smpc_export_sample_trajectories", "smpc_run_control_loop", "smpc_run_control_loops", "smpc_set_x0",
     "smpc_launch_iteration", "smpc_synchronize", "smpc_stream", "smpc_kernels_per_solve",
-    "smpc_rollout_kernel_ms", "smpc_icdf_domain", "smpc_icdf_table", "smpc_comm_unique_id", "smpc_comm_init", "smpc_comm_set_mode", "smpc_group_init",
+    "smpc_rollout_kernel_ms", "smpc_icdf_domain", "smpc_icdf_table", "smpc_comm_unique_id", "smpc_comm_init", "smpc_comm_set_mode", "smpc_set_injected_noise", "smpc_group_init",
     "smpc_group_compute_control", "smpc_host_libm_uses_fma",
     "smpc_measure_fp32_peak", "smpc_sqrt_check", "smpc_libm_hash", "smpc_fast_math_check", "smpc_select_noise_strategy", "smpc_noise_strategy_rule",
     "smpc_version",
@@ -108,6 +108,8 @@ def load(path: str = None) -> ctypes.CDLL:
     L.smpc_icdf_table.argtypes = [c_ctx, f32p]
     L.smpc_comm_unique_id.argtypes = [ctypes.c_char_p]
     L.smpc_comm_init.argtypes = [c_ctx, ctypes.c_char_p, ctypes.c_int32, ctypes.c_int32]
+    L.smpc_set_injected_noise.argtypes = [c_ctx, ctypes.c_void_p]
+    L.smpc_set_injected_noise.restype = ctypes.c_int
     L.smpc_comm_set_mode.argtypes = [c_ctx, ctypes.c_int32]
     L.smpc_comm_set_mode.restype = ctypes.c_int
     L.smpc_group_init.argtypes = [P(c_ctx), ctypes.c_int32]

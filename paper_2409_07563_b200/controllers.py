@@ -260,6 +260,12 @@ class MppiController(RolloutEngine):
     def comm_init(self, unique_id: bytes, rank: int, world: int) -> None:
         self._check(self.lib.smpc_comm_init(self.ctx, unique_id, rank, world))
 
+    def set_injected_noise(self, device_ptr: int) -> None:
+        """Injected-noise mode: later solves read the shard's [M_local, T, n_u]
+        fp32 noise from this DEVICE pointer (e.g. a CUDA tensor's data_ptr());
+        0 returns to the Philox sampler. The caller keeps the buffer alive."""
+        self._check(self.lib.smpc_set_injected_noise(self.ctx, ctypes.c_void_p(int(device_ptr)) if device_ptr else None))
+
     def comm_set_mode(self, mode: str) -> None:
         """"single" (default): one all-gather per iteration; "exact": three."""
         self._check(self.lib.smpc_comm_set_mode(self.ctx, COMM_MODES[mode]))

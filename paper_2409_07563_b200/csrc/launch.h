@@ -212,6 +212,13 @@ struct IterArgs {
   // and sums them in the reference's order. A sample whose fast chain flags
   // is replayed exactly by the rollout kernel (rflag[i] = 1, its J written).
   int split;
+  // Injected noise staged by TMA (cp.async.bulk.tensor 2-D, 128 samples x 32
+  // floats per box, SWIZZLE_128B) into double-buffered shared memory: the
+  // host-side CUtensorMap (launch passes it by value) and whether it is valid
+  // (eps rows 16-byte multiples).
+  const void* eps_map;
+  int eps_tma;
+  int tu4;  // T * n_u % 4 == 0: float4 reads of injected eps rows
   float* ytraj;
   float* utraj;
   unsigned char* rflag;

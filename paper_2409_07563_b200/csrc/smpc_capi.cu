@@ -2,6 +2,7 @@
 // with the reference's error texts, device buffers, the captured per-solve
 // CUDA graph, the engine/sampler boundary calls and NCCL multi-GPU plumbing.
 // Host code only — all arithmetic on the hot path runs in the kernels.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <math.h>
@@ -169,6 +170,12 @@ struct smpc_ctx {
   int rank = 0, world = 1;
   int comm_mode = SMPC_COMM_SINGLE;  // one all-gather per iteration (smpc_comm_set_mode)
   double* d_gather_rec = nullptr;    // [8][rec] packed per-rank records of the single-collective mode
+  // injected noise (device [M_local][T][n_u]) for every solve, and the TMA
+  // descriptors of it and of the engine-boundary copy d_eps
+  const float* d_inj = nullptr;
+  alignas(64) CUtensorMap inj_map;
+  alignas(64) CUtensorMap eps_map;
+  bool inj_tma = false, eps_tma = false;
   double* d_rm_score = nullptr;      // RMPPI candidate scratch (warp-cooperative models)
   float* d_rm_z = nullptr;
   // host state
@@ -363,6 +370,35 @@ uint32_t tail_table_size(uint32_t* j_lo_out, uint32_t* j_hi_out);
 
 int gather_record(const smpc_ctx* c) { return 4 * c->S + c->S * c->T * c->nu; }
 
+// TMA descriptor of an injected-noise tensor [rows][T*n_u] fp32 (reference
+// layout, sampling.hpp:40-42): boxes of 32 floats x 128 rows, SWIZZLE_128B
+// (the rollout kernel's tma_src). false when the rows are not 16-byte
+// multiples or the driver entry point is unavailable (checked per-step path).
+bool encode_eps_map(CUtensorMap* map, const float* d, long long rows, int tu) {
+  if (tu % 4 != 0 || rows < 1) return false;
+  typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                               CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static EncodeFn encode = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      encode = (EncodeFn)fn;
+  }
+  if (!encode) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)tu, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)tu * sizeof(float)};
+  const cuuint32_t box[2] = {32, (cuuint32_t)kRolloutThreads};
+  const cuuint32_t estr[2] = {1, 1};
+  return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(d), dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // normal_icdf over the sampler's whole 2^23-point domain, one 32 MB table per
 // device shared by every context (it depends on nothing but the arithmetic),
 // built by the same icdf_quad_words path the kernels evaluate in registers.
@@ -437,6 +473,9 @@ void fill_args(smpc_ctx* c) {
   a.rm_score = c->d_rm_score;
   a.rm_z = c->d_rm_z;
   a.split = 0;  // enabled per launch with the split-noise buffer (enqueue_solve)
+  a.eps_map = nullptr;
+  a.eps_tma = 0;
+  a.tu4 = (c->T * c->nu) % 4 == 0;
   a.ytraj = c->d_ytraj;
   a.utraj = c->d_utraj;
   a.rflag = c->d_rflag;
@@ -618,7 +657,11 @@ void enqueue_solve(smpc_ctx* c, bool timed) {
     a.iter = it;
     a.do_finish = it == c->I - 1;
     if (timed) CK(cudaEventRecord(c->ev[2 * it], c->stream));
-    if (c->use_zq) {  // split noise: one parallel pass, off the per-sample serial chain
+    if (c->d_inj) {  // injected noise (smpc_set_injected_noise): rollout and update read it
+      a.eps_in = c->d_inj;
+      a.eps_tma = c->inj_tma;
+      a.eps_map = &c->inj_map;
+    } else if (c->use_zq) {  // split noise: one parallel pass, off the per-sample serial chain
       a.zq = c->d_zq;
       a.split = c->d_ytraj ? c->split_sb : 0;  // and the split dynamics / cost rollout
       CK(launch_gen_zq(a, c->nu, c->d_zq, c->stream));
@@ -1360,9 +1403,13 @@ smpc_status smpc_rollout(smpc_ctx* c, int32_t S, const float* x0s, const float* 
         if (c->d_eps) cudaFree(c->d_eps);
         c->d_eps = dalloc<float>(n);
         c->eps_cap = n;
+        c->eps_tma = false;  // re-encode for the new buffer
       }
       CK(cudaMemcpyAsync(c->d_eps, eps, sizeof(float) * n, cudaMemcpyHostToDevice, c->stream));
+      if (!c->eps_tma) c->eps_tma = encode_eps_map(&c->eps_map, c->d_eps, c->M_local, (int)TU);
       a.eps_in = c->d_eps;
+      a.eps_tma = c->eps_tma;
+      a.eps_map = &c->eps_map;
     }
     if (outputs_out) {
       const size_t n = (size_t)S * c->M_local * c->T * c->ny;
@@ -1526,9 +1573,13 @@ smpc_status smpc_export_sample_trajectories(smpc_ctx* c, const float* x0, const 
         if (c->d_eps) cudaFree(c->d_eps);
         c->d_eps = dalloc<float>(n);
         c->eps_cap = n;
+        c->eps_tma = false;  // re-encode for the new buffer
       }
       CK(cudaMemcpyAsync(c->d_eps, eps, sizeof(float) * n, cudaMemcpyHostToDevice, c->stream));
+      if (!c->eps_tma) c->eps_tma = encode_eps_map(&c->eps_map, c->d_eps, c->M_local, (int)TU);
       a.eps_in = c->d_eps;
+      a.eps_tma = c->eps_tma;
+      a.eps_map = &c->eps_map;
     }
     // 1) the fused rollout (RolloutResult::costs, system 0)
     CK(launch_begin_solve(c->header(), c->stream));
@@ -1895,6 +1946,20 @@ smpc_status smpc_comm_unique_id(uint8_t id_out[128]) {
   if (api->GetUniqueId(&id) != 0) return SMPC_ERR_CUDA;
   memcpy(id_out, id.internal, 128);
   return SMPC_OK;
+}
+
+smpc_status smpc_set_injected_noise(smpc_ctx* c, const float* d_eps) {
+  if (!c) return SMPC_ERR_ARGUMENT;
+  return guarded(c, [&] {
+    if (c->p.controller_kind == SMPC_CTRL_CEM || c->p.dynamics_kind == SMPC_DYN_MLP)
+      throw ConfigError{"injected noise: supported for mppi / dmd / tube / rmppi on the SIMT models"};
+    c->d_inj = d_eps;
+    c->inj_tma = d_eps ? encode_eps_map(&c->inj_map, d_eps, c->M_local, c->T * c->nu) : false;
+    if (c->graph) {
+      cudaGraphExecDestroy(c->graph);
+      c->graph = nullptr;
+    }
+  });
 }
 
 smpc_status smpc_comm_set_mode(smpc_ctx* c, int32_t mode) {
