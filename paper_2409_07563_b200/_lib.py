@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(HERE, "libsmpc_b200.so")
 
 # Every symbol include/smpc_b200.h declares (checked by tests/test_capi_symbols.py).
 EXPORTED = [
-    "smpc_create", "smpc_destroy", "smpc_last_error", "smpc_error_location", "smpc_get_dims",
+    "smpc_create", "smpc_create_with_ops", "smpc_destroy", "smpc_last_error", "smpc_error_location", "smpc_get_dims",
     "smpc_set_mean", "smpc_get_mean", "smpc_compute_control", "smpc_tube_compute_control",
     "smpc_shift_control_sequence", "smpc_get_solve_count", "smpc_set_solve_count",
     "smpc_generate_samples", "smpc_rollout", "smpc_compute_weights", "smpc_sorted_samples", "smpc_export_sample_trajectories", "smpc_run_control_loop", "smpc_run_control_loops", "smpc_set_x0",
@@ -30,6 +30,29 @@ EXPORTED = [
 ]
 
 _lib = None
+
+
+# smpc_model_ops (include/smpc_b200.h): a user model's launcher table
+_OPS_FN = ctypes.CFUNCTYPE(ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p)
+
+
+class SmpcModelOps(ctypes.Structure):
+    _fields_ = [
+        ("abi_version", ctypes.c_int32),
+        ("args_bytes", ctypes.c_int32),
+        ("n_x", ctypes.c_int32),
+        ("n_u", ctypes.c_int32),
+        ("n_y", ctypes.c_int32),
+        ("name", ctypes.c_char_p),
+        ("user", ctypes.c_void_p),
+        ("user_bytes", ctypes.c_int64),
+        ("rollout", ctypes.c_void_p),
+        ("update", ctypes.c_void_p),
+        ("combine", ctypes.c_void_p),
+        ("generate", ctypes.c_void_p),
+        ("plant_step", ctypes.c_void_p),
+        ("rmppi_select", ctypes.c_void_p),
+    ]
 
 
 class SmpcError(RuntimeError):
@@ -70,6 +93,8 @@ def load(path: str = None) -> ctypes.CDLL:
     f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
     u8p = np.ctypeslib.ndpointer(np.uint8, flags="C_CONTIGUOUS")
     L.smpc_create.argtypes = [P(SmpcProblem), P(c_ctx)]
+    L.smpc_create_with_ops.argtypes = [P(SmpcProblem), P(SmpcModelOps), P(c_ctx)]
+    L.smpc_create_with_ops.restype = ctypes.c_int
     L.smpc_destroy.argtypes = [c_ctx]
     L.smpc_destroy.restype = None
     L.smpc_last_error.argtypes = [c_ctx]

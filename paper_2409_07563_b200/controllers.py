@@ -65,12 +65,18 @@ class TubeSolution:
 class _Context:
     """Owns one smpc_ctx (device buffers + captured CUDA graph)."""
 
-    def __init__(self, scenario: Scenario, shard: Optional[tuple] = None):
+    def __init__(self, scenario: Scenario, shard: Optional[tuple] = None, ops=None):
+        """ops: a user model's smpc_model_ops (SmpcModelOps, from a plugin
+        compiled against include/smpc_b200_plugin.cuh) for dynamics="plugin"."""
         self.lib = _lib.load()
         self.scenario = scenario
         self._problem = scenario.to_problem(shard)
         self.ctx = ctypes.c_void_p()
-        check(self.lib.smpc_create(ctypes.byref(self._problem), ctypes.byref(self.ctx)))
+        if ops is not None:
+            self._ops = ops
+            check(self.lib.smpc_create_with_ops(ctypes.byref(self._problem), ctypes.byref(ops), ctypes.byref(self.ctx)))
+        else:
+            check(self.lib.smpc_create(ctypes.byref(self._problem), ctypes.byref(self.ctx)))
         nx, nu, ny = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
         self.lib.smpc_get_dims(self.ctx, ctypes.byref(nx), ctypes.byref(nu), ctypes.byref(ny))
         self.n_x, self.n_u, self.n_y = nx.value, nu.value, ny.value
@@ -291,12 +297,13 @@ class TubeMppiController(MppiController):
 COMM_MODES = {"exact": 0, "single": 1}
 
 
-def make_controller(scenario: Scenario, shard: Optional[tuple] = None) -> MppiController:
-    """make_controller (controllers.cpp:294-344): mppi | dmd | cem | tube (+ rmppi, builder-defined)."""
+def make_controller(scenario: Scenario, shard: Optional[tuple] = None, ops=None) -> MppiController:
+    """make_controller (controllers.cpp:294-344): mppi | dmd | cem | tube (+ rmppi, builder-defined).
+    ops: a user model's smpc_model_ops for scenario.dynamics == "plugin"."""
     if scenario.controller in ("tube", "rmppi"):
-        return TubeMppiController(scenario, shard)
+        return TubeMppiController(scenario, shard, ops)
     if scenario.controller in ("mppi", "dmd", "cem"):
-        return MppiController(scenario, shard)
+        return MppiController(scenario, shard, ops)
     raise SmpcConfigError(2, f"controller.kind '{scenario.controller}' is not recognized")
 
 

@@ -50,7 +50,7 @@ struct Problem {
 
 /// ScenarioConfig (scenario.hpp:118-140) -> smpc_problem, with the same
 /// kind strings as make_dynamics / make_cost / make_controller.
-inline Problem make_problem(const ScenarioConfig& sc, int device = 0) {
+inline Problem make_problem(const ScenarioConfig& sc, int device = 0, bool plugin = false) {
   Problem out;
   smpc_problem& p = out.p;
   p.abi_version = SMPC_B200_ABI_VERSION;
@@ -85,7 +85,9 @@ inline Problem make_problem(const ScenarioConfig& sc, int device = 0) {
   p.nominal_reset_bound = sc.controller.nominal_reset_bound;
   p.elite_fraction = sc.controller.elite_fraction;
   const DynamicsSection& d = sc.dynamics;
-  if (d.kind == "unicycle") {
+  if (plugin) {  // a user model: its device functors carry the model and cost (smpc_create_with_ops)
+    p.dynamics_kind = SMPC_DYN_PLUGIN;
+  } else if (d.kind == "unicycle") {
     p.dynamics_kind = SMPC_DYN_UNICYCLE;
   } else if (d.kind == "cartpole") {
     p.dynamics_kind = SMPC_DYN_CARTPOLE;
@@ -103,7 +105,8 @@ inline Problem make_problem(const ScenarioConfig& sc, int device = 0) {
     throw ConfigError("dynamics.kind '" + d.kind + "' is not recognized");
   }
   const CostSection& c = sc.cost;
-  if (c.kind == "road") {
+  if (plugin) {
+  } else if (c.kind == "road") {
     p.cost_kind = SMPC_COST_ROAD;
     const double v[] = {c.road_half_width, c.road_linear_coeff, c.road_quadratic_coeff};
     p.n_cost_params = 3;
@@ -161,6 +164,21 @@ class GpuMppiController : public Controller {
  public:
   GpuMppiController(const ScenarioConfig& scenario, int device = 0, double update_skip_mass = 0.0)
       : GpuMppiController(scenario, make_problem(scenario, device), update_skip_mass) {}
+
+  /// A user model: the user's own reference-side DynamicsModel / CostFunction
+  /// subclasses (dynamics.hpp:17-74, costs.hpp:16-37 — Plant and
+  /// SimulatedSystem keep using them) plus their device twins compiled
+  /// against include/smpc_b200_plugin.cuh (ops, from smpc_ops_for). The
+  /// scenario supplies the sampler / controller / plant sections.
+  GpuMppiController(std::shared_ptr<const DynamicsModel> dynamics, std::shared_ptr<const CostFunction> cost,
+                    const ScenarioConfig& scenario, const smpc_model_ops& ops, int device = 0,
+                    double update_skip_mass = 0.0)
+      : Controller(scenario.controller.kind, dynamics, std::move(cost),
+                   make_sampler_config(scenario, dynamics->dims().n_u), settings_from(scenario), single_worker()),
+        problem_(make_problem(scenario, device, true)) {
+    problem_.p.update_skip_mass = update_skip_mass;
+    check(smpc_create_with_ops(&problem_.p, &ops, &ctx_), nullptr);
+  }
 
   ~GpuMppiController() override { smpc_destroy(ctx_); }
   GpuMppiController(const GpuMppiController&) = delete;

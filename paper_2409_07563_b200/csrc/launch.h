@@ -244,6 +244,10 @@ struct IterArgs {
   // Indexed rollout (export_sample_trajectories re-roll): thread i rolls out
   // global sample sample_idx[i] (nullptr: m_begin + i)
   const long long* sample_idx;
+  // user-model plugin (smpc_create_with_ops): the smpc_model_ops table and
+  // the context's copy of its functor pair, read by the host trampolines
+  const void* plugin_ops;
+  const void* plugin_user;
   // Small-N mode: the iteration's standard-normal quads pre-generated by
   // gen_zq_kernel, [Q][M_local] float4 (nullptr: regenerate in the rollout)
   const float4* zq;
@@ -270,6 +274,7 @@ ModelOps ops_diff_drive(bool fma_libm);
 ModelOps ops_double_integrator();
 ModelOps ops_quadrotor();
 ModelOps ops_mlp(bool fma_libm);
+ModelOps ops_plugin();  // trampolines into IterArgs::plugin_ops (smpc_capi.cu)
 ModelOps ops_bicycle(bool fma_libm);
 
 cudaError_t launch_select(const IterArgs& a, SelectState* st, long long k, unsigned int* counters, int* eq_cnt,

@@ -173,6 +173,8 @@ struct smpc_ctx {
   // injected noise (device [M_local][T][n_u]) for every solve, and the TMA
   // descriptors of it and of the engine-boundary copy d_eps
   const float* d_inj = nullptr;
+  smpc_model_ops plugin{};            // user model (smpc_create_with_ops), with its functor pair copied
+  std::vector<unsigned char> plugin_user;
   alignas(64) CUtensorMap inj_map;
   alignas(64) CUtensorMap eps_map;
   bool inj_tma = false, eps_tma = false;
@@ -231,6 +233,27 @@ double pc(const smpc_problem& p, int i, double d) { return i < p.n_cost_params ?
 // Controller ctor (controllers.cpp:23-49), GaussianSampler ctor
 // (sampling.cpp:7-30), model ctors (dynamics.cpp:133-171), cost ctors and
 // make_cost (costs.cpp:27-162), RolloutEngine::validate (engine.cpp:81-127).
+// ---- user-model plugin trampolines (smpc_create_with_ops) --------------------
+const smpc_model_ops* plugin_of(const IterArgs& a) { return static_cast<const smpc_model_ops*>(a.plugin_ops); }
+cudaError_t plugin_rollout(const IterArgs& a, int, cudaStream_t st) {
+  return (cudaError_t)plugin_of(a)->rollout(&a, a.plugin_user, st);
+}
+cudaError_t plugin_rmppi(const IterArgs& a, int, cudaStream_t st) {
+  return (cudaError_t)plugin_of(a)->rmppi_select(&a, a.plugin_user, st);
+}
+cudaError_t plugin_plant(const IterArgs& a, int, const PlantStepArgs& p, cudaStream_t st) {
+  return (cudaError_t)plugin_of(a)->plant_step(&a, a.plugin_user, &p, st);
+}
+cudaError_t plugin_update(const IterArgs& a, cudaStream_t st) {
+  return (cudaError_t)plugin_of(a)->update(&a, a.plugin_user, st);
+}
+cudaError_t plugin_combine(const IterArgs& a, cudaStream_t st) {
+  return (cudaError_t)plugin_of(a)->combine(&a, a.plugin_user, st);
+}
+cudaError_t plugin_generate(const IterArgs& a, float* e, uint8_t* f, cudaStream_t st) {
+  return (cudaError_t)plugin_of(a)->generate(&a, a.plugin_user, e, f, st);
+}
+
 void validate(smpc_ctx* c) {
   const smpc_problem& p = c->p;
   if (p.abi_version != SMPC_B200_ABI_VERSION) throw ConfigError{"smpc_problem: ABI version mismatch"};
@@ -268,6 +291,17 @@ void validate(smpc_ctx* c) {
         throw RuntimeError{"bicycle: control bound lower must be < upper on channel 1"};
       c->ops = ops_bicycle(c->fma);
       break;
+    case SMPC_DYN_PLUGIN: {  // user functors (smpc_create_with_ops): launchers from the plugin
+      const smpc_model_ops& o = c->plugin;
+      if (o.abi_version != SMPC_B200_ABI_VERSION || o.args_bytes != (int32_t)sizeof(IterArgs))
+        throw ConfigError{"smpc_model_ops: built against a different library version"};
+      if (!o.rollout || !o.update || !o.combine || !o.generate || !o.plant_step)
+        throw ConfigError{"smpc_model_ops: missing launcher"};
+      if (o.n_x < 1 || o.n_u < 1 || o.n_y < 1) throw ConfigError{"smpc_model_ops: invalid dimensions"};
+      c->ops = ModelOps{plugin_rollout, o.rmppi_select ? plugin_rmppi : nullptr, plugin_plant, launch_weights,
+                        plugin_update, plugin_combine, plugin_generate, o.n_x, o.n_u, o.n_y};
+      break;
+    }
     case SMPC_DYN_MLP:  // builder-defined (models.cuh:MlpDyn, tcgen05 rollout in mlp.cu)
       if (!p.dyn_tensor || p.dyn_tensor_len != mlp_layout::TOTAL)
         throw RuntimeError{"mlp: dyn_tensor must hold " + std::to_string(mlp_layout::TOTAL) +
@@ -282,10 +316,11 @@ void validate(smpc_ctx* c) {
   if (p.controller_kind != SMPC_CTRL_MPPI && p.controller_kind != SMPC_CTRL_DMD &&
       p.controller_kind != SMPC_CTRL_TUBE && p.controller_kind != SMPC_CTRL_CEM && p.controller_kind != SMPC_CTRL_RMPPI)
     throw ConfigError{"controller.kind is not recognized"};
-  // cost (make_cost + ctor checks)
+  // cost (make_cost + ctor checks); a plugin's cost functor is its own
   int cost_ny = c->ny, cost_nu = c->nu;
   std::string cost_name;
-  switch (p.cost_kind) {
+  switch (p.dynamics_kind == SMPC_DYN_PLUGIN ? -1 : p.cost_kind) {
+    case -1: cost_name = "plugin"; break;
     case SMPC_COST_ROAD:
       cost_name = "road";
       if (c->ny < 2) throw RuntimeError{"road cost needs at least 2 output channels"};
@@ -317,9 +352,11 @@ void validate(smpc_ctx* c) {
   }
   static const char* dyn_names[] = {"unicycle", "cartpole", "diff_drive", "double_integrator", "quadrotor", "mlp",
                                     "bicycle"};
+  const char* dyn_name = p.dynamics_kind == SMPC_DYN_PLUGIN ? (c->plugin.name ? c->plugin.name : "plugin")
+                                                             : dyn_names[p.dynamics_kind];
   if (cost_ny != c->ny)
     throw ConfigError{"cost '" + cost_name + "' expects " + std::to_string(cost_ny) +
-                      " output channels but model '" + dyn_names[p.dynamics_kind] + "' produces " +
+                      " output channels but model '" + dyn_name + "' produces " +
                       std::to_string(c->ny)};
   if (cost_nu != c->nu) throw RuntimeError{"rollout request cost dimensions do not match the model"};
   // sampler
@@ -369,6 +406,8 @@ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 uint32_t tail_table_size(uint32_t* j_lo_out, uint32_t* j_hi_out);
 
 int gather_record(const smpc_ctx* c) { return 4 * c->S + c->S * c->T * c->nu; }
+
+
 
 // TMA descriptor of an injected-noise tensor [rows][T*n_u] fp32 (reference
 // layout, sampling.hpp:40-42): boxes of 32 floats x 128 rows, SWIZZLE_128B
@@ -472,6 +511,8 @@ void fill_args(smpc_ctx* c) {
   a.cost_threshold = p.cost_threshold;
   a.rm_score = c->d_rm_score;
   a.rm_z = c->d_rm_z;
+  a.plugin_ops = p.dynamics_kind == SMPC_DYN_PLUGIN ? &c->plugin : nullptr;
+  a.plugin_user = c->plugin_user.empty() ? nullptr : c->plugin_user.data();
   a.split = 0;  // enabled per launch with the split-noise buffer (enqueue_solve)
   a.eps_map = nullptr;
   a.eps_tma = 0;
@@ -573,6 +614,7 @@ void fill_args(smpc_ctx* c) {
       break;
     }
     case SMPC_COST_DIFF_DRIVE_NAV: {
+      if (p.dynamics_kind == SMPC_DYN_PLUGIN) break;
       const double d[6] = {2.0, 2.0, 0.0, 5.0, 5.0, 20.0};
       for (int i = 0; i < 6; ++i) cp.p[i] = (float)pc(p, i, d[i]);
       cp.grid = c->d_costmap;
@@ -588,6 +630,15 @@ void fill_args(smpc_ctx* c) {
       cp.n_quad = p.n_quad;
       for (int i = 0; i < p.n_quad; ++i) cp.target[i] = p.quad_target[i], cp.weights[i] = p.quad_weights[i];
       break;
+  }
+  if (p.dynamics_kind == SMPC_DYN_PLUGIN && c->d_costmap) {  // a plugin cost with USES_MAP reads the problem's map
+    cp.grid = c->d_costmap;
+    cp.cells_x = p.costmap_cells_x;
+    cp.cells_y = p.costmap_cells_y;
+    cp.origin_x = (float)p.costmap_origin_x;
+    cp.origin_y = (float)p.costmap_origin_y;
+    cp.inv_resolution = (float)(1.0 / p.costmap_resolution);
+    cp.map_in_smem = (size_t)cp.cells_x * cp.cells_y <= 96 * 1024;
   }
 }
 
@@ -952,11 +1003,31 @@ extern "C" {
 
 const char* smpc_version(void) { return "paper_2409_07563_b200 0.1 (sm_100a)"; }
 
-smpc_status smpc_create(const smpc_problem* problem, smpc_ctx** out) {
+static smpc_status create_impl(const smpc_problem* problem, const smpc_model_ops* ops, smpc_ctx** out);
+
+smpc_status smpc_create(const smpc_problem* problem, smpc_ctx** out) { return create_impl(problem, nullptr, out); }
+
+smpc_status smpc_create_with_ops(const smpc_problem* problem, const smpc_model_ops* ops, smpc_ctx** out) {
+  if (!ops) return SMPC_ERR_ARGUMENT;
+  return create_impl(problem, ops, out);
+}
+
+static smpc_status create_impl(const smpc_problem* problem, const smpc_model_ops* ops, smpc_ctx** out) {
   if (!problem || !out) return SMPC_ERR_ARGUMENT;
   *out = nullptr;
   smpc_ctx* c = new smpc_ctx();
   c->p = *problem;
+  if (ops) {
+    c->plugin = *ops;
+    if (ops->user && ops->user_bytes > 0)
+      c->plugin_user.assign((const unsigned char*)ops->user, (const unsigned char*)ops->user + ops->user_bytes);
+    c->plugin.user = c->plugin_user.empty() ? nullptr : c->plugin_user.data();
+    c->p.dynamics_kind = SMPC_DYN_PLUGIN;
+  } else if (problem->dynamics_kind == SMPC_DYN_PLUGIN) {
+    g_create_error = "dynamics.kind plugin needs smpc_create_with_ops";
+    delete c;
+    return SMPC_ERR_CONFIG;
+  }
   c->fma = smpc_host_libm_uses_fma() != 0;
   const smpc_status st = guarded(nullptr, [&] {
     validate(c);
@@ -1090,7 +1161,8 @@ smpc_status smpc_create(const smpc_problem* problem, smpc_ctx** out) {
       c->base.sig2_pow2 = pow2 ? 1 : 0;  // fill_args leaves it alone
     }
     CK(cudaMemcpy(c->d_gamma, gam.data(), sizeof(double) * c->T, cudaMemcpyHostToDevice));
-    if (p.cost_kind == SMPC_COST_DIFF_DRIVE_NAV) {
+    if ((p.dynamics_kind != SMPC_DYN_PLUGIN && p.cost_kind == SMPC_COST_DIFF_DRIVE_NAV) ||
+        (p.dynamics_kind == SMPC_DYN_PLUGIN && !c->costmap.empty())) {
       const size_t cells = (size_t)p.costmap_cells_x * p.costmap_cells_y;
       c->d_costmap = dalloc<uint8_t>(cells);
       if (!c->costmap.empty()) CK(cudaMemcpy(c->d_costmap, c->costmap.data(), cells, cudaMemcpyHostToDevice));

@@ -23,7 +23,9 @@ ABI_VERSION = 3
 
 DYNAMICS_KINDS = {"unicycle": 0, "cartpole": 1, "diff_drive": 2, "double_integrator": 3,
                   # builder-defined (no reference counterpart): BASELINE.json configs[1] / configs[3]
-                  "quadrotor": 4, "mlp": 5, "bicycle": 6}
+                  "quadrotor": 4, "mlp": 5, "bicycle": 6,
+                  # a user model compiled against include/smpc_b200_plugin.cuh (smpc_create_with_ops)
+                  "plugin": 100}
 COST_KINDS = {"road": 0, "circle_track": 1, "diff_drive_nav": 2, "quadratic": 3}
 CONTROLLER_KINDS = {"mppi": 0, "dmd": 1, "cem": 2, "tube": 3, "rmppi": 4}
 
@@ -242,6 +244,8 @@ class Scenario:
     dt_min: float = 0.02
     disturbance_std: float = 0.0
     device: int = 0
+    # user model (dynamics="plugin"): (n_x, n_u, n_y) of the plugin's functors
+    plugin_dims: Optional[Sequence[int]] = None
     # B200 deployment knob (not in the reference schema): weighted-update
     # samples with w_m < update_skip_mass / M are skipped (0 = exact).
     update_skip_mass: float = 2.0 ** -64
@@ -249,10 +253,12 @@ class Scenario:
     # --- derived -----------------------------------------------------------
     @property
     def dims(self):
+        if self.dynamics == "plugin":
+            return tuple(int(v) for v in self.plugin_dims)
         return MODEL_DIMS[self.dynamics]
 
     def x0(self) -> np.ndarray:
-        names = STATE_NAMES[self.dynamics]
+        names = STATE_NAMES.get(self.dynamics) or [f"X{i}" for i in range(self.dims[0])]
         x = np.zeros(len(names), np.float32)
         for k, v in self.initial_state.items():
             x[names.index(k)] = np.float32(v)
@@ -351,7 +357,7 @@ class Scenario:
         p.n_dyn_params = len(dp)
         for i, v in enumerate(dp):
             p.dyn_params[i] = float(v)
-        p.cost_kind = COST_KINDS[self.cost]
+        p.cost_kind = COST_KINDS.get(self.cost, 0)
         cp = self._cost_params()
         p.n_cost_params = len(cp)
         for i, v in enumerate(cp):

@@ -19,6 +19,8 @@ from paper_2409_07563_b200 import scenario as S
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 BIN = os.path.join(ROOT, "build", "drop_in_plant")
+BIN_PLUGIN = os.path.join(ROOT, "build", "drop_in_plugin")
+PLUGIN_LIB = os.path.join(ROOT, "tests", "native", "libuser_model.so")
 
 
 def build_drop_in():
@@ -34,6 +36,11 @@ def build_drop_in():
            "-L", os.path.join(ROOT, "paper_2409_07563_b200"), "-lsmpc_b200",
            "-Wl,-rpath,$ORIGIN/../oracle/_ref:$ORIGIN/../paper_2409_07563_b200", "-pthread"]
     subprocess.run(cmd, check=True)
+    # a user model on both sides: reference subclasses + the out-of-tree device plugin
+    cmd = [c if c != os.path.join(ROOT, "tests", "native", "drop_in_plant.cpp")
+           else os.path.join(ROOT, "tests", "native", "drop_in_plugin.cpp") for c in cmd]
+    cmd[cmd.index("-o") + 1] = BIN_PLUGIN
+    subprocess.run(cmd + ["-ffp-contract=off", "-ldl"], check=True)
     return True
 
 
@@ -87,3 +94,27 @@ def test_reference_plant_drives_gpu_controller(tmp_path, name):
     assert xr.shape == xg.shape
     assert np.allclose(xg[:5], xr[:5], rtol=1e-4, atol=1e-5)
     assert abs(gpu["accumulated_cost"] - ref["accumulated_cost"]) <= 1e-3 * max(1.0, abs(ref["accumulated_cost"]))
+
+
+@pytest.mark.gpu
+def test_reference_plant_drives_user_model_plugin():
+    """The user's own DynamicsModel / CostFunction subclasses (spring-mass)
+    run by the unmodified reference MppiController, and the same model's
+    device twin (out-of-tree plugin, include/smpc_b200_plugin.cuh) run by
+    GpuMppiController: identical first solve (the Philox noise, the model's
+    IEEE ops and the softmin baseline reproduce bit for bit; U* within the
+    FP32 tolerance), then the reference Plant closed loop on both."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    if not (os.path.exists(BIN_PLUGIN) and os.path.exists(PLUGIN_LIB)):
+        pytest.skip("plugin drop-in binary not built (needs /root/reference at build time)")
+    r = subprocess.run([BIN_PLUGIN, PLUGIN_LIB, "0.4"], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr
+    ref, gpu = [json.loads(ln) for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert gpu["rho"] == ref["rho"] and gpu["argmax_w"] == ref["argmax_w"]
+    assert abs(gpu["eta"] - ref["eta"]) <= 1e-9 * max(1.0, ref["eta"])
+    assert np.allclose(gpu["u"], ref["u"], rtol=1e-4, atol=1e-5)
+    assert gpu["solves"] == ref["solves"]
+    xr, xg = np.array(ref["x"]), np.array(gpu["x"])
+    assert xr.shape == xg.shape and np.allclose(xg, xr, rtol=1e-4, atol=1e-5)
