@@ -96,6 +96,45 @@ __device__ __forceinline__ f2 tanh2(f2 x) {
   return pk(copysignf(r0, a), copysignf(r1, b));
 }
 
+// Two tanh on the FMA pipe only (no MUFU): the clamped odd rational
+// x P(x^2) / Q(x^2) (degree 13 / 6, the minimax form Eigen uses for float
+// tanh; abs error ~1e-7 on the clamp range, where tanh saturates to 1 in
+// float), the division by Q in [4.9e-3, 1] as an integer-seeded reciprocal
+// with three Newton steps. The layer-2 epilogue mixes it with tanh2 so the
+// XU (ex2 + rcp) and FMA pipes share the 64 tanh per sample-step.
+__device__ __forceinline__ f2 tanh2_fma(f2 x) {
+#define SPL(c) f2splat_bits(__float_as_uint(c))
+  float a, b;
+  f2unpack(x, a, b);
+  const float lim = 7.90531110763549805f;
+  a = fminf(fmaxf(a, -lim), lim);
+  b = fminf(fmaxf(b, -lim), lim);
+  const f2 xc = pk(a, b);
+  const f2 x2 = fma2(xc, xc, 0ull);
+  f2 p = fma2(x2, SPL(-2.76076847742355e-16f), SPL(2.00018790482477e-13f));
+  p = fma2(x2, p, SPL(-8.60467152213735e-11f));
+  p = fma2(x2, p, SPL(5.12229709037114e-08f));
+  p = fma2(x2, p, SPL(1.48572235717979e-05f));
+  p = fma2(x2, p, SPL(6.37261928875436e-04f));
+  p = fma2(x2, p, SPL(4.89352455891786e-03f));
+  p = fma2(xc, p, 0ull);
+  f2 q = fma2(x2, SPL(1.19825839466702e-06f), SPL(1.18534705686654e-04f));
+  q = fma2(x2, q, SPL(2.26843463243900e-03f));
+  q = fma2(x2, q, SPL(4.89352518554385e-03f));
+  float q0, q1;
+  f2unpack(q, q0, q1);
+  f2 r = pk(__uint_as_float(0x7EF311C3u - __float_as_uint(q0)), __uint_as_float(0x7EF311C3u - __float_as_uint(q1)));
+  const f2 nq = q ^ 0x8000000080000000ull;  // -q
+#pragma unroll
+  for (int it = 0; it < 3; ++it) r = fma2(r, fma2(nq, r, SPL(1.0f)), r);  // r += r (1 - q r)
+#undef SPL
+  return fma2(p, r, 0ull);
+}
+
+#ifndef SMPC_MLP_FMA_TANH
+#define SMPC_MLP_FMA_TANH 1  // layer-2 epilogue: every other tanh pair on the FMA pipe (A/B: 0 = all MUFU)
+#endif
+
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
@@ -350,7 +389,7 @@ __global__ void __launch_bounds__(RM ? 2 * kTile : kTile, RM ? 2 : 4)
     for (int j = 0; j < HID; j += 2) {
       const f2 hb = fma2(pk(d2[j], d2[j + 1]), f2splat_bits(0x3F800000u), *reinterpret_cast<const f2*>(sB2 + j));
       float h0, h1;
-      f2unpack(tanh2(hb), h0, h1);
+      f2unpack((SMPC_MLP_FMA_TANH && ((j >> 1) & 1)) ? tanh2_fma(hb) : tanh2(hb), h0, h1);
       const ulonglong2 w0 = *reinterpret_cast<const ulonglong2*>(sW3 + j * OUT);        // W3T[j][0..3]
       const ulonglong2 w1 = *reinterpret_cast<const ulonglong2*>(sW3 + (j + 1) * OUT);  // W3T[j+1][0..3]
       const f2 hh0 = pk(h0, h0), hh1 = pk(h1, h1);
