@@ -274,7 +274,12 @@ def bench_config(workload: str, n_global: int, world: int, sc, comm: str) -> dic
 
 
 def run_reference_arm(args):
-    rank, world, local, dist = init_dist(args.gpus)
+    # the reference is a CPU library: no process group; under torchrun only
+    # rank 0 times it and prints, the other ranks exit without work
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if rank != 0:
         return
     n_global = args.samples * (world if args.scaling == "weak" else 1)
