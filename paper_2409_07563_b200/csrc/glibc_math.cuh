@@ -17,6 +17,13 @@
 // -fmad says); the host build (used only by the exhaustive CPU check) must be
 // compiled with -ffp-contract=off. Exhaustive equality against the host libm
 // over all 2^32 float inputs: tests/test_glibc_math.py.
+//
+// Third-party notice. The algorithms and constant tables restated here come
+// from glibc 2.39 (sysdeps/ieee754/flt-32: e_logf.c, s_sinf.c, s_cosf.c,
+// sincosf.h, e_logf_data.c, s_sincosf_data.c), which takes them from ARM's
+// optimized-routines. glibc is licensed LGPL-2.1-or-later; optimized-routines
+// is MIT OR Apache-2.0 WITH LLVM-exception. This file is a restatement of
+// those routines and carries their licences; see THIRD_PARTY_NOTICES.md.
 #pragma once
 
 #include <math.h>
