@@ -198,6 +198,8 @@ struct IterArgs {
   int n_u_blocks;
   double* blk_part;      // [S][QG][upd_slots][QW][4] per-warp quad sums, by rank among the group's warps
   int upd_slots;         // max warps covering one quad group
+  unsigned int* upd_gcnt;  // [S][QG] warps done per quad group (self-resetting)
+  double* upd_gsum;      // [S][QG][QW][4] reduced quad-group sums (written by each group's last warp)
   double* gather3;       // [world][S][T*NU]
   // per-rank strides (doubles) of gather1/2/3: separate buffers in the exact
   // three-collective mode; one packed record [g1 | g2 | g3] per rank in the

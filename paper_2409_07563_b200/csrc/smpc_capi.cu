@@ -119,6 +119,8 @@ struct smpc_ctx {
   float *d_mean = nullptr, *d_x0 = nullptr, *d_sigma = nullptr, *d_tail = nullptr;
   double *d_sig2 = nullptr, *d_gamma = nullptr, *d_costs = nullptr, *d_weights = nullptr;
   double *d_blk_min = nullptr, *d_blk_eta = nullptr, *d_blk_part = nullptr;
+  double* d_upd_gsum = nullptr;
+  unsigned int* d_upd_gcnt = nullptr;
   double *d_gather1 = nullptr, *d_gather2 = nullptr, *d_gather3 = nullptr;
   int *d_cand = nullptr, *d_cand_cnt = nullptr;
   double* d_cand_e = nullptr;
@@ -556,6 +558,8 @@ void fill_args(smpc_ctx* c) {
   a.cand_off = c->d_cand_off;
   a.n_u_blocks = c->n_u_blocks;
   a.blk_part = c->d_blk_part;
+  a.upd_gsum = c->d_upd_gsum;
+  a.upd_gcnt = c->d_upd_gcnt;
   a.gather3 = c->d_gather3;
   a.comm_single = c->comm_mode == SMPC_COMM_SINGLE;
   if (a.comm_single) {  // one record per rank: [S][2] (rho, argmin) | [S][2] (eta, nz) | [S][T*NU] sums
@@ -1101,6 +1105,8 @@ static smpc_status create_impl(const smpc_problem* problem, const smpc_model_ops
       // warps covering one quad group: <= 2 * warps / QG + 2 (each owns >= U / (2 W) units)
       c->upd_slots = (int)(2 * ((warps + QG - 1) / QG) + 3);
       c->d_blk_part = dalloc<double>((size_t)c->S * QG * c->upd_slots * kUpdateSlot);
+      c->d_upd_gsum = dalloc<double>((size_t)c->S * QG * kUpdateSlot);
+      c->d_upd_gcnt = dalloc<unsigned int>((size_t)c->S * QG);
     }
     c->d_counters = dalloc<unsigned int>(16);
     c->d_select = dalloc<SelectState>(1);
@@ -1228,7 +1234,7 @@ void smpc_destroy(smpc_ctx* c) {
                   c->d_ro_x0, c->d_ro_mean, c->d_eps, c->d_outputs, c->d_wscratch, c->d_flags,
                   c->d_cand, c->d_cand_e, c->d_cand_cnt, c->d_cand_off, c->d_select, c->d_eq_cnt, c->d_eq_off,
                   c->d_dyn_tensor, c->d_zq, c->d_gather_rec, c->d_rm_score, c->d_rm_z,
-                  c->d_ytraj, c->d_utraj, c->d_rflag};
+                  c->d_ytraj, c->d_utraj, c->d_rflag, c->d_upd_gsum, c->d_upd_gcnt};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->h_result) cudaFreeHost(c->h_result);

@@ -17,7 +17,11 @@ LIB = os.path.join(HERE, "native", "libuser_model.so")
 
 def build_user_model(force: bool = False) -> str:
     """nvcc the out-of-tree plugin (sm_100a) next to its source."""
-    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(SRC):
+    import glob
+    deps = [SRC] + glob.glob(os.path.join(ROOT, "include", "*")) + glob.glob(
+        os.path.join(ROOT, "paper_2409_07563_b200", "csrc", "*.cuh")) + [
+        os.path.join(ROOT, "paper_2409_07563_b200", "csrc", "launch.h")]
+    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(d) for d in deps):
         subprocess.run(["nvcc", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo",
                         "-fmad=false", "-Xcompiler", "-fPIC", "-shared", "-I", os.path.join(ROOT, "include"), "-I",
                         os.path.join(ROOT, "paper_2409_07563_b200", "csrc"), SRC, "-o", LIB], check=True)
