@@ -1,3 +1,7 @@
+#!/bin/bash
+# Phase timing of the update kernel (main loop / last-CTA commit / finish) per
+# workload. Requires an instrumented build in build/timing/ (globaltimer
+# printf in the update kernel's tail; not part of the product build).
 for w in "cartpole 2048" "quadrotor 8192" "paper 2048" "di 1048576" "autorally_rmppi 8192"; do
   set -- $w
   echo "== $1 $2"
