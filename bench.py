@@ -144,7 +144,7 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
+        sm, mx, reasons, pw = [], None, set(), []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
@@ -155,11 +155,15 @@ class ClockSampler:
                 mx = float(parts[1])
             except ValueError:
                 continue
+            try:
+                pw.append(float(parts[2]))
+            except ValueError:
+                pass
             for nm, v in zip(names, parts[4:8]):
                 if v.lower() == "active":
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "power_w": statistics.median(pw) if pw else None}
 
 
 def init_dist(want: int):
@@ -404,43 +408,59 @@ def measure(ctl, sc, workload, n_global, shard, steps, warmup, roofline_steps, e
 def run_sweep(args, device, flush, fp32_peak):
     """Every BASELINE config (+ the reference's timing protocol over N) on one
     GPU, with the reference CPU path on this host at 1 thread and all threads."""
-    from paper_2409_07563_b200.controllers import make_controller
     out = []
     for workload, n in SWEEP:
-        sc = make_scenario(workload, n)
-        sc.device = device
-        ctl = make_controller(sc)
-        small = n <= 16384
-        r = measure(ctl, sc, workload, n, (0, n), steps=200 if small else 50, warmup=10, roofline_steps=20,
-                    e2e_steps=100 if small else 30, device=device, flush=flush, dist=None, local=0,
-                    fp32_peak=fp32_peak)
-        ctl.close()
-        ent = {"workload": workload_name(workload, n), "key": f"{workload}:{n}", "samples": n,
-               "horizon": sc.horizon, "ms_per_iter": r["ms_per_step"], "samples_per_s": r["value"],
-               "p50_ms": statistics.median(r["step_ms"]), "p99_ms": float(np.percentile(r["step_ms"], 99)),
-               "e2e_ms": r["e2e"]["ms_per_step"], "rollout_ms": r["roofline"]["kernel_ms"],
-               "rollout_frac_fp32_issue": r["roofline"]["frac"], "gpu_launches_per_iter": r["launches"] // 200
-               if small else r["launches"] // 50}
-        if "tensor" in r["roofline"]:
-            ent["tensor_tf32_tflops"] = r["roofline"]["tensor"]["achieved"]
-            ent["tensor_frac"] = r["roofline"]["tensor"]["frac"]
-        if not args.no_cpu_baseline:
-            ref = workload in REFERENCE_WORKLOADS
-            cpu = {}
-            for w in ([1, 0] if ref else [1]):
-                c = cpu_reference_run(sc, steps=5, warmup=1 if ref else 0, budget_s=args.sweep_cpu_budget,
-                                      prefer_ref=ref, workers=w)
-                cpu[f"w{c['cores']}"] = {"ms_per_iter": c["ms"], "samples_per_s": c["value"], "kind": c["kind"],
-                                         "solves": c["n"]}
-            ent["cpu"] = cpu
-            best = min(v["ms_per_iter"] for v in cpu.values())
-            ent["speedup_e2e_vs_best_cpu"] = best / r["e2e"]["ms_per_step"]
-            if not ref:
-                ent["cpu_note"] = "builder-defined model: no reference implementation; CPU figure is its " \
-                                  "restated C twin (oracle port, 1 thread), parity unpinned"
-        out.append(ent)
-    out.append(injected_entry(args, device, flush, fp32_peak))
+        try:
+            out.append(sweep_entry(args, device, flush, fp32_peak, workload, n))
+        except Exception as e:  # one failing entry must not take the bench line with it
+            out.append({"workload": workload_name(workload, n), "key": f"{workload}:{n}", "samples": n,
+                        "error": f"{type(e).__name__}: {e}"})
+    try:
+        out.append(injected_entry(args, device, flush, fp32_peak))
+    except Exception as e:
+        out.append({"key": "di_injected:1048576", "error": f"{type(e).__name__}: {e}"})
     return out
+
+
+def sweep_entry(args, device, flush, fp32_peak, workload, n):
+    from paper_2409_07563_b200.controllers import make_controller
+    sc = make_scenario(workload, n)
+    sc.device = device
+    ctl = make_controller(sc)
+    small = n <= 16384
+    try:
+        with ClockSampler(device) as clocks:
+            r = measure(ctl, sc, workload, n, (0, n), steps=200 if small else 50, warmup=10, roofline_steps=20,
+                        e2e_steps=100 if small else 30, device=device, flush=flush, dist=None, local=0,
+                        fp32_peak=fp32_peak)
+    finally:
+        ctl.close()
+    clk = clocks.summary()
+    ent = {"workload": workload_name(workload, n), "key": f"{workload}:{n}", "samples": n,
+           "horizon": sc.horizon, "ms_per_iter": r["ms_per_step"], "samples_per_s": r["value"],
+           "p50_ms": statistics.median(r["step_ms"]), "p99_ms": float(np.percentile(r["step_ms"], 99)),
+           "e2e_ms": r["e2e"]["ms_per_step"], "rollout_ms": r["roofline"]["kernel_ms"],
+           "rollout_frac_fp32_issue": r["roofline"]["frac"], "gpu_launches_per_iter": r["launches"] // 200
+           if small else r["launches"] // 50,
+           "clocks": {"sm_mhz": clk["sm_mhz"], "reasons": clk["reasons"], "power_w": clk.get("power_w")}}
+    if "tensor" in r["roofline"]:
+        ent["tensor_tf32_tflops"] = r["roofline"]["tensor"]["achieved"]
+        ent["tensor_frac"] = r["roofline"]["tensor"]["frac"]
+    if not args.no_cpu_baseline:
+        ref = workload in REFERENCE_WORKLOADS
+        cpu = {}
+        for w in ([1, 0] if ref else [1]):
+            c = cpu_reference_run(sc, steps=5, warmup=1 if ref else 0, budget_s=args.sweep_cpu_budget,
+                                  prefer_ref=ref, workers=w)
+            cpu[f"w{c['cores']}"] = {"ms_per_iter": c["ms"], "samples_per_s": c["value"], "kind": c["kind"],
+                                     "solves": c["n"]}
+        ent["cpu"] = cpu
+        best = min(v["ms_per_iter"] for v in cpu.values())
+        ent["speedup_e2e_vs_best_cpu"] = best / r["e2e"]["ms_per_step"]
+        if not ref:
+            ent["cpu_note"] = "builder-defined model: no reference implementation; CPU figure is its " \
+                              "restated C twin (oracle port, 1 thread), parity unpinned"
+    return ent
 
 
 def measured_hbm_peak():

@@ -1144,7 +1144,7 @@ static smpc_status create_impl(const smpc_problem* problem, const smpc_model_ops
       memset(&h, 0, sizeof h);
       h.err_key = kNoError;
       h.abort_key = kNoError;
-      CK(cudaMemcpy(c->d_result, &h, sizeof h, cudaMemcpyHostToDevice));
+      CK(cudaMemcpyAsync(c->d_result, &h, sizeof h, cudaMemcpyHostToDevice, c->stream));
     }
     // sigma / sigma^2 (sampling.hpp:56-60, sampling.cpp:123) and gamma (engine.cpp:397-401)
     std::vector<float> sig(TU);
@@ -1159,19 +1159,19 @@ static smpc_status create_impl(const smpc_problem* problem, const smpc_model_ops
       }
     for (int t = 0; t < c->T; ++t)
       gam[t] = c->step_sizes.empty() ? 1.0 : (double)c->step_sizes[c->step_sizes.size() == 1 ? 0 : t];
-    CK(cudaMemcpy(c->d_sigma, sig.data(), sizeof(float) * TU, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(c->d_sig2, sig2.data(), sizeof(double) * TU, cudaMemcpyHostToDevice));
+    CK(cudaMemcpyAsync(c->d_sigma, sig.data(), sizeof(float) * TU, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->d_sig2, sig2.data(), sizeof(double) * TU, cudaMemcpyHostToDevice, c->stream));
     {
       bool pow2 = true;
       for (double v : sig2) pow2 = pow2 && exact_inverse_pow2(v) != 0.0;
       c->base.sig2_pow2 = pow2 ? 1 : 0;  // fill_args leaves it alone
     }
-    CK(cudaMemcpy(c->d_gamma, gam.data(), sizeof(double) * c->T, cudaMemcpyHostToDevice));
+    CK(cudaMemcpyAsync(c->d_gamma, gam.data(), sizeof(double) * c->T, cudaMemcpyHostToDevice, c->stream));
     if ((p.dynamics_kind != SMPC_DYN_PLUGIN && p.cost_kind == SMPC_COST_DIFF_DRIVE_NAV) ||
         (p.dynamics_kind == SMPC_DYN_PLUGIN && !c->costmap.empty())) {
       const size_t cells = (size_t)p.costmap_cells_x * p.costmap_cells_y;
       c->d_costmap = dalloc<uint8_t>(cells);
-      if (!c->costmap.empty()) CK(cudaMemcpy(c->d_costmap, c->costmap.data(), cells, cudaMemcpyHostToDevice));
+      if (!c->costmap.empty()) CK(cudaMemcpyAsync(c->d_costmap, c->costmap.data(), cells, cudaMemcpyHostToDevice, c->stream));
     }
     if (p.dynamics_kind == SMPC_DYN_MLP) {  // + W2 transposed for the warp-cooperative nominal rollout
       using namespace mlp_layout;
@@ -1180,7 +1180,7 @@ static smpc_status create_impl(const smpc_problem* problem, const smpc_model_ops
     }
     if (!dyn_tensor.empty()) {
       c->d_dyn_tensor = dalloc<float>(dyn_tensor.size());
-      CK(cudaMemcpy(c->d_dyn_tensor, dyn_tensor.data(), sizeof(float) * dyn_tensor.size(), cudaMemcpyHostToDevice));
+      CK(cudaMemcpyAsync(c->d_dyn_tensor, dyn_tensor.data(), sizeof(float) * dyn_tensor.size(), cudaMemcpyHostToDevice, c->stream));
     }
     uint32_t j_lo, j_hi;
     tail_table_size(&j_lo, &j_hi);
@@ -1198,6 +1198,11 @@ static smpc_status create_impl(const smpc_problem* problem, const smpc_model_ops
       CK(cudaCreateTextureObject(&tex, &rd, &td, nullptr));
       c->tail_tex = (unsigned long long)tex;
     }
+    // Creation-time uploads are ordered on the context's (non-blocking) stream
+    // and complete before the first solve: a pageable cudaMemcpy may return
+    // before its DMA lands and is not ordered with a non-blocking stream (a
+    // solve could read the zeroed result header, i.e. a spurious error key).
+    CK(cudaStreamSynchronize(c->stream));
     c->host_mean[0].assign(TU, 0.f);
     c->host_mean[1].assign(TU, 0.f);
     c->nominal_state.assign(c->nx, 0.f);

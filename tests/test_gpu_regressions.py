@@ -53,3 +53,23 @@ def test_shift_is_ordered_after_a_launched_iteration(mods):
     b.launch_iteration()
     b.shift_control_sequence(3 * sc.dt, sc.dt)
     assert np.array_equal(b.mean(), want)
+
+
+def test_first_solve_after_create_sees_initialised_state(mods):
+    """Creation-time uploads (result header with its no-error key, sigma,
+    gamma, costmap, model tensors) are ordered on the context's non-blocking
+    stream and complete before the first solve: a pageable cudaMemcpy could
+    return before its DMA landed, and a solve launched right away read the
+    zeroed header as error key 0 ("non-finite state channel 0 at sample 0
+    timestep 0"; seen once in a bench sweep). Contexts are created and solved
+    back to back, with the previous context's memory freed just before."""
+    S, C = mods["S"], mods["C"]
+    builders = [lambda: S.cartpole_scenario(num_samples=2048, horizon=100, seed=1),
+                lambda: S.di_swarm_scenario(num_samples=65536, horizon=100, seed=7)]
+    for k in range(40):
+        sc = builders[k % 2]()
+        ctl = C.make_controller(sc)
+        ctl.set_x0(sc.x0())
+        ctl.launch_iteration()
+        ctl.synchronize()  # raises on a spurious error key
+        ctl.close()
