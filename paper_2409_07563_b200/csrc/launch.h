@@ -288,7 +288,6 @@ cudaError_t launch_begin_solve(ResultHeader* h, cudaStream_t stream);
 cudaError_t launch_shift_mean(float* mean, int S, int T, int NU, long long steps, cudaStream_t stream);
 cudaError_t launch_gen_zq(const IterArgs& a, int nu, float4* zq, cudaStream_t stream);
 cudaError_t launch_icdf_domain(const IterArgs& a, float* out, cudaStream_t stream);
-cudaError_t launch_finish_solve(ResultHeader* h, cudaStream_t stream);
 cudaError_t launch_weights(const IterArgs& a, cudaStream_t stream);
 cudaError_t launch_normalize_weights(const IterArgs& a, cudaStream_t stream);
 cudaError_t launch_min_only(const double* costs, long long n, double* blk_min, long long* blk_arg,

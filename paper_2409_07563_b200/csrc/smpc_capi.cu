@@ -754,7 +754,6 @@ void enqueue_solve(smpc_ctx* c, bool timed) {
       CK(c->ops.combine(a, c->stream));
     }
   }
-  CK(launch_finish_solve(c->header(), c->stream));
 }
 
 // ---- in-process shard group (one host thread, any devices) ------------------
@@ -809,7 +808,6 @@ void enqueue_group_solve(smpc_ctx** cs, int n) {
     group_allgather(cs, n, single ? 0 : 3);
     for (int r = 0; r < n; ++r) CK(cs[r]->ops.combine(args(cs[r]), cs[r]->stream));
   }
-  for (int r = 0; r < n; ++r) CK(launch_finish_solve(cs[r]->header(), cs[r]->stream));
 }
 
 void build_graph(smpc_ctx* c) {
@@ -1768,8 +1766,9 @@ int32_t smpc_kernels_per_solve(const smpc_ctx* c) {
   if (!c) return 0;
   const int zq = c->use_zq ? 1 : 0;  // gen_zq_kernel per iteration in split-noise mode
   const int rm = c->p.controller_kind == SMPC_CTRL_RMPPI ? 1 : 0;
-  if (c->p.controller_kind == SMPC_CTRL_CEM) return 2 + c->I * (1 + 11 + 1 + zq);  // rollout, select (init+8+2), update
-  return 2 + rm + c->I * (3 + zq + (c->world > 1 ? 1 : 0));
+  // begin_solve + per iteration (the clean-solve count is kept by the last update / combine)
+  if (c->p.controller_kind == SMPC_CTRL_CEM) return 1 + c->I * (1 + 11 + 1 + zq);  // rollout, select (init+8+2), update
+  return 1 + rm + c->I * (3 + zq + (c->world > 1 ? 1 : 0));
 }
 
 smpc_status smpc_icdf_table(smpc_ctx* c, float* out) {

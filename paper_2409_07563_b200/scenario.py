@@ -19,7 +19,7 @@ import numpy as np
 
 SMPC_MAX_DIM = 16
 SMPC_MAX_PARAMS = 32
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 DYNAMICS_KINDS = {"unicycle": 0, "cartpole": 1, "diff_drive": 2, "double_integrator": 3,
                   # builder-defined (no reference counterpart): BASELINE.json configs[1] / configs[3]
