@@ -230,6 +230,7 @@ struct IterArgs {
   float* states;    // [S][T+1][NX]
   float* outs_nom;  // [S][T][NY]
   int do_finish;    // final iteration of a solve: nominal rollout + solve_count++
+  int begin_keys;   // this kernel opens the solve: reset the error / abort keys (no begin_solve launch)
   int normalize_weights;  // write w = e/eta back (only when the caller wants weights)
   double skip_w;          // update skips samples with w_m < skip_w (0 = exact)
   double cem_k;           // CEM: elite count k (commit mean + acc / k); 0 = MPPI / Tube

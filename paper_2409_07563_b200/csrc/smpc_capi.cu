@@ -702,7 +702,9 @@ void decode_error(smpc_ctx* c, unsigned long long key) {
 
 // One solve's device work on c->stream (graph-captured or direct).
 void enqueue_solve(smpc_ctx* c, bool timed) {
-  CK(launch_begin_solve(c->header(), c->stream));
+  // small-N mode: the first gen_zq resets the error keys itself
+  const bool zq_opens = c->use_zq && !c->d_inj && c->p.controller_kind != SMPC_CTRL_RMPPI;
+  if (!zq_opens) CK(launch_begin_solve(c->header(), c->stream));
   if (c->p.controller_kind == SMPC_CTRL_RMPPI) {  // nominal-state choice, once per solve
     IterArgs a = c->base;
     CK(c->ops.rmppi_select(a, c->p.cost_kind, c->stream));
@@ -719,7 +721,9 @@ void enqueue_solve(smpc_ctx* c, bool timed) {
     } else if (c->use_zq) {  // split noise: one parallel pass, off the per-sample serial chain
       a.zq = c->d_zq;
       a.split = c->d_ytraj ? c->split_sb : 0;  // and the split dynamics / cost rollout
-      CK(launch_gen_zq(a, c->nu, c->d_zq, c->stream));
+      IterArgs g = a;
+      g.begin_keys = zq_opens && it == 0;
+      CK(launch_gen_zq(g, c->nu, c->d_zq, c->stream));
     }
     CK(c->ops.rollout(a, c->p.cost_kind, c->stream));
     if (timed) CK(cudaEventRecord(c->ev[2 * it + 1], c->stream));
@@ -1766,9 +1770,11 @@ int32_t smpc_kernels_per_solve(const smpc_ctx* c) {
   if (!c) return 0;
   const int zq = c->use_zq ? 1 : 0;  // gen_zq_kernel per iteration in split-noise mode
   const int rm = c->p.controller_kind == SMPC_CTRL_RMPPI ? 1 : 0;
-  // begin_solve + per iteration (the clean-solve count is kept by the last update / combine)
-  if (c->p.controller_kind == SMPC_CTRL_CEM) return 1 + c->I * (1 + 11 + 1 + zq);  // rollout, select (init+8+2), update
-  return 1 + rm + c->I * (3 + zq + (c->world > 1 ? 1 : 0));
+  // begin_solve (folded into the first gen_zq in small-N mode) + per iteration
+  // (the clean-solve count is kept by the last update / combine)
+  const int begin = c->use_zq && !c->d_inj && !rm ? 0 : 1;
+  if (c->p.controller_kind == SMPC_CTRL_CEM) return begin + c->I * (1 + 11 + 1 + zq);  // rollout, select (init+8+2), update
+  return begin + rm + c->I * (3 + zq + (c->world > 1 ? 1 : 0));
 }
 
 smpc_status smpc_icdf_table(smpc_ctx* c, float* out) {
